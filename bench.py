@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 divide-and-conquer sampler (arXiv 1610.05141).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+                    [--workload headline|cfg1|cfg0|complement|bernoulli|wr]
+
+One "step" = one pass of the whole hot path over one sample: the split tree,
+the leaves and the stores, plus, for N > 1, the NCCL
+all-gather of per-GPU counts.  Default workload: rs_sample_wor for
+n = 2^32 per GPU from N = 2^48 (the north-star headline at N = 1; weak
+scaling "n = p * 2^32" at N > 1), seed 1.  Inputs are three scalars, so they
+are "resident" by construction; the 32 GiB output per GPU is far larger than
+the 126 MB L2, so no L2 flush is needed between steps.
+
+Prints ONE JSON line on rank 0 (metric/value/unit/..., roofline, cpu_baseline,
+e2e, clocks, gpu_launches).  --impl reference times the CPU oracle (the only
+reference this tier has) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sorted samples/sec and output HBM GB/s vs peak at 1/2/4/8 B200"
+UNIT = "samples/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _workload(name, world):
+    from paper_1610_05141_b200 import workloads as W
+    if name == "headline":
+        n = world * W.HEADLINE["n"]
+        wl = "wor_n2^32_N2^48" if world == 1 else f"weak_wor_n2^32perGPU_N2^48_p{world}"
+        return dict(name=wl, mode="wor", N=W.HEADLINE["N"], n=n, seed=1)
+    if name == "weak30":
+        return dict(name=f"weak_wor_n2^30perGPU_N2^48_p{world}", mode="wor", N=2 ** 48,
+                    n=world * 2 ** 30, seed=1)
+    if name == "cfg1":
+        return dict(W.CFG1)
+    if name == "cfg0":
+        return dict(W.CFG0)
+    if name == "complement":
+        return dict(W.CFG3A)
+    if name == "bernoulli":
+        return dict(W.CFG3B_ROOF)
+    if name == "bernoulli32":
+        return dict(W.CFG3B)
+    if name == "wr":
+        return dict(W.CFG4)
+    raise SystemExit(f"unknown workload {name}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+        self.t0 = self.t1 = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu=timestamp,{self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is not None:
+            time.sleep(0.12)
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        try:
+            self.f.seek(0)
+            rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        except Exception:
+            rows = []
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                r = [x.strip() for x in r]
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for nm, v in zip(names, r[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+            except Exception:
+                continue
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _max_over_ranks(x, world, device):
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle timings (cpu_baseline leg and --impl reference)
+# ---------------------------------------------------------------------------
+
+def oracle_sample(wl, target_s=10.0, leaf_start=0):
+    """Time the oracle (as it stands) on a bounded sample of the workload:
+    a contiguous run of output leaves (found by path replay) or Bernoulli
+    chunks, sized for ~target_s seconds on all host cores."""
+    import oracle as O
+    cores = os.cpu_count() or 1
+    if wl["mode"] == "bernoulli":
+        N, rho = wl["N"], wl["rho"]
+        nch = 1 << O.bern_depth(N, rho)
+        t = time.perf_counter(); _, v = O.bern_chunks_digest(N, rho, wl["seed"], 0, 64)
+        rate = v / max(time.perf_counter() - t, 1e-6)
+        chunks = int(min(nch, max(64, rate * target_s / max(v / 64, 1))))
+        t = time.perf_counter(); _, v = O.bern_chunks_digest(N, rho, wl["seed"], 0, chunks)
+        dt = time.perf_counter() - t
+        return dict(value=v / dt, unit=UNIT, cores=1, kind="oracle",
+                    sample=f"first {chunks} of {nch} Bernoulli chunks of {wl['name']} ({v} values, "
+                           f"{dt:.1f} s, single-threaded oracle)")
+    mode = O.MODE_WR if wl["mode"] == "wr" else O.MODE_WOR
+    N, n = wl["N"], wl["n"]
+    D = O.plan(N, n, mode)[0]
+    nl = 1 << D
+    probe = min(nl, 256)
+    t = time.perf_counter()
+    _, v = O.digest_leaves_replay(N, n, wl["seed"], mode, leaf_start, leaf_start + probe, cores)
+    dt = time.perf_counter() - t
+    leaves = int(min(nl - leaf_start, max(probe, probe * target_s / max(dt, 1e-6))))
+    t = time.perf_counter()
+    _, v = O.digest_leaves_replay(N, n, wl["seed"], mode, leaf_start, leaf_start + leaves, cores)
+    dt = time.perf_counter() - t
+    return dict(value=v / dt, unit=UNIT, cores=cores, kind="oracle",
+                sample=f"leaves [{leaf_start},{leaf_start + leaves}) of {nl} of {wl['name']} "
+                       f"({v} values by path replay, {dt:.1f} s, {cores} threads)")
+
+
+def run_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    wl = _workload(args.workload, world)
+    steps = []
+    # each step = a bounded sample of the same workload (distinct leaves)
+    per_step_s = max(1.0, min(20.0, 120.0 / max(args.steps + args.warmup, 1)))
+    base = None
+    for i in range(args.warmup + args.steps):
+        r = oracle_sample(wl, target_s=per_step_s)
+        if i >= args.warmup:
+            steps.append(r["value"])
+        base = r
+    val = sorted(steps)[len(steps) // 2] if steps else base["value"]
+    out = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": wl["name"], "N": wl["N"], "n": wl.get("n"), "rho": wl.get("rho"),
+                   "seed": wl["seed"], "impl_note": "CPU oracle (oracle/rso.c), bounded sample per step"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": base["cores"], "kind": "oracle",
+                         "sample": base["sample"]},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# native (GPU) arm
+# ---------------------------------------------------------------------------
+
+def run_native(args):
+    import paper_1610_05141_b200 as rs
+    world, rank, local = _dist()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    wl = _workload(args.workload, world)
+    mode = wl["mode"]
+    stream = torch.cuda.current_stream()
+
+    # ---- buffers (outside the timed region)
+    if mode == "bernoulli":
+        N, rho, seed = wl["N"], wl["rho"], wl["seed"]
+        cap = rs.bernoulli_capacity(N, rho)
+        local_cap = cap if world == 1 else (cap // world + 64 * int(math.sqrt(cap)) + 64)
+        out = torch.empty(local_cap, dtype=torch.uint64, device=dev)
+        cnt = torch.zeros(1, dtype=torch.uint64, device=dev)
+        ws = torch.empty(rs.workspace_bytes(rs.MODE_BERNOULLI, N, 0, rho, world), dtype=torch.uint8,
+                         device=dev)
+        n_local_expected = None
+
+        def step():
+            rs.bernoulli_ws(N, rho, seed, world, rank, out, local_cap, cnt, ws)
+            if world > 1:
+                allc = torch.empty(world, dtype=torch.int64, device=dev)
+                dist.all_gather_into_tensor(allc, cnt.view(torch.int64))
+    else:
+        N, n, seed = wl["N"], wl["n"], wl["seed"]
+        m = rs.MODE_WR if mode == "wr" else rs.MODE_WOR
+        n_local, g_off = rs.shard_info(N, n, seed, world, rank, m)
+        out = torch.empty(max(n_local, 1), dtype=torch.uint64, device=dev)
+        ws = torch.empty(rs.workspace_bytes(m, N, n, 0.0, world), dtype=torch.uint8, device=dev)
+        cnt = torch.tensor([n_local], dtype=torch.int64, device=dev)
+        fn = rs.sample_wr_ws if m == rs.MODE_WR else rs.sample_wor_ws
+        allc = torch.empty(world, dtype=torch.int64, device=dev)
+
+        def step():
+            fn(N, n, seed, world, rank, out, ws)
+            if world > 1:
+                dist.all_gather_into_tensor(allc, cnt)   # per-GPU counts -> global offsets
+
+    # ---- warm-up (untimed)
+    for _ in range(max(args.warmup, 3 if args.warmup >= 3 else args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    rs.timing_enable(True)
+    rs.timing_read(reset=True)
+    rs.launch_count(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = rs.launch_count(reset=True)
+    rs.timing_enable(False)
+    kt = rs.timing_read(reset=True)
+    clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_max = _max_over_ranks(ms, world, dev)
+
+    # ---- correctness of what was timed (untimed): sizes, order, range
+    if mode == "bernoulli":
+        c_local = int(cnt.item())
+        assert c_local <= local_cap, "bernoulli capacity exceeded"
+        bad = rs.validate(out[:c_local], N, strict=True)
+        n_local_done = c_local
+    else:
+        bad = rs.validate(out[:n_local], N, strict=(mode != "wr"))
+        n_local_done = n_local
+        if world > 1:
+            off = int(allc[:rank].sum().item())
+            assert off == g_off, "all-gathered offset disagrees with the Algorithm P replay"
+    assert bad == 0, f"validation failed: {bad} bad values"
+    assert rs.device_errors(clear=True) == 0, "device capacity flag raised"
+    total = torch.tensor([n_local_done], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(total)
+    n_total = float(total.item())
+
+    value = n_total / (ms_max / 1e3)
+    gbs = 8.0 * n_total / (ms_max / 1e3) / 1e9
+
+    # ---- roofline of the dominant kernel (leaf / Bernoulli), live CUDA events
+    peak, peak_src = _peaks()
+    if mode == "bernoulli":
+        kms, kl = kt["bernoulli"]
+        nunits = 1 << (rs.plan(rs.MODE_BERNOULLI, N, 0, rho)[0])
+        bytes_per_launch = 8.0 * n_local_done + 8.0 * nunits / world
+        kname = "k_bernoulli"
+    else:
+        kms, kl = kt["leaf"]
+        D = rs.plan(m, N, n)[0]
+        nleaves = (1 << D) // world
+        bytes_per_launch = 8.0 * n_local + 12.0 * nleaves
+        kname = "k_leaf_comp32" if (mode == "wor" and rs.plan(m, N, n)[1]) else (
+            "k_leaf_wr32" if mode == "wr" else "k_leaf_wor32")
+    kms_per = kms / max(kl, 1)
+    achieved = bytes_per_launch / (kms_per / 1e3) / 1e9 if kms_per > 0 else None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(wl["name"])
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "kernel": kname, "kernel_ms": kms_per, "peak_source": peak_src,
+                "step_share": kms / max(args.steps, 1) / ms if ms > 0 else None,
+                "split_ms": kt["split"][0] / max(args.steps, 1)}
+
+    # ---- end to end through the C ABI with a host buffer (fewer steps)
+    e2e = None
+    if not args.no_e2e and mode != "bernoulli":
+        try:
+            try:
+                host = torch.empty(max(n_local, 1), dtype=torch.uint64, pin_memory=True)
+                pinned = True
+            except Exception:
+                host = torch.empty(max(n_local, 1), dtype=torch.uint64)
+                pinned = False
+            rs.sample_shard_host(m, N, n, seed, world, rank, host)        # warm-up
+            reps = args.e2e_steps
+            if world > 1:
+                dist.barrier()
+            t = time.perf_counter()
+            for _ in range(reps):
+                rs.sample_shard_host(m, N, n, seed, world, rank, host)
+                if world > 1:
+                    dist.all_gather_into_tensor(allc, cnt)
+            torch.cuda.synchronize()
+            dt = (time.perf_counter() - t) / reps
+            dt = _max_over_ranks(dt, world, dev)
+            e2e = {"value": n_total / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": int(8 * n_total), "pinned": pinned, "steps": reps,
+                   "note": "rs_sample_shard_host: device generation + D2H of the whole sample"}
+            del host
+        except Exception as ex:  # report, never fake
+            e2e = {"value": None, "unit": UNIT, "error": str(ex)[:200]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = oracle_sample(wl, target_s=args.cpu_seconds)
+        except Exception as ex:
+            cpu = {"value": None, "error": str(ex)[:200]}
+
+    if rank == 0:
+        res = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u64", "data": "synthetic",
+            "config": {"workload": wl["name"], "N": wl["N"], "n": wl.get("n"), "rho": wl.get("rho"),
+                       "seed": wl["seed"], "parallelism": f"shard{world}",
+                       "l2": "output >> 126 MB L2 (no flush needed)" if n_total * 8 > 1e9
+                       else "output smaller than L2 (cache-warm)"},
+            "output_gbs": gbs, "output_frac_of_peak": gbs / peak,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clocks.summary(), "gpu_launches": launches,
+        }
+        print(json.dumps(res))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--workload", default="headline")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_native(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,161 @@
+/*
+ * rs.h -- C ABI of librs.so, the B200 (sm_100a) divide-and-conquer random
+ * sampler of Sanders, Lamm, Huebschle-Schneider, Schrade and Dachsbacher,
+ * "Efficient Random Sampling -- Parallel, Vectorized, Cache-Efficient, and
+ * Online" (arXiv 1610.05141).  P:n = /root/reference/PAPER.md line n.
+ *
+ * Conventions (all entry points):
+ *  - Values are 1-based uint64, little-endian, ascending; "sorted sample of
+ *    n numbers out of the range 1..N".
+ *  - Pointers named *_dev / out are DEVICE pointers owned by the caller
+ *    (e.g. allocated by torch); the library owns only its transient
+ *    workspace (stream-ordered cudaMallocAsync, or the caller's via *_ws).
+ *  - Calls are asynchronous on `stream` (cudaStream_t passed as void*;
+ *    NULL = legacy default stream).  Argument errors are detected on the
+ *    host before any launch and nothing is written.
+ *  - Results are a pure function of (N, n or rho, seed): identical for any
+ *    world size and bit-exact with the CANON v1 definition.
+ *  - No CPU fallback: without a CUDA device every call returns RS_ECUDA.
+ *  - Thread-safe and reentrant; no global RNG state (the seed is an
+ *    argument).  rs_last_status() is thread-local.
+ *  - Device-side capacity overflows (a leaf needing more than the
+ *    on-chip capacity -- probability < 1e-100 at every supported shape,
+ *    DESIGN.md 5) raise a sticky device flag read by rs_device_errors().
+ */
+#ifndef RS_H
+#define RS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RS_OK = 0,
+    RS_EINVAL = 1,     /* invalid argument (n > N, rho not in [0,1], ...) */
+    RS_ECUDA = 2,      /* CUDA runtime error / no device                  */
+    RS_ENOMEM = 3,     /* workspace allocation failed / too small         */
+    RS_ECAPACITY = 4   /* output capacity exceeded (Bernoulli)            */
+} rs_status;
+
+enum { RS_MODE_WOR = 0, RS_MODE_WR = 1, RS_MODE_BERNOULLI = 2 };
+
+/* ---- sampling without replacement: Algorithm R / P ----------
+ * Writes the n distinct values of a uniform random n-subset of 1..N to
+ * out[0..n), ascending.  out: device, capacity >= n.  n > N -> RS_EINVAL;
+ * n == 0 -> no-op; N >= 2^63 -> RS_EINVAL.  If 2n > N the N-n values NOT in
+ * the sample are generated and the complement is emitted. */
+rs_status rs_sample_wor(uint64_t N, uint64_t n, uint64_t seed, uint64_t *out, void *stream);
+
+/* ---- sampling with replacement: binomial splits ------------
+ * n values of 1..N with repeats (iid uniform), ascending.  N == 0 && n > 0
+ * -> RS_EINVAL. */
+rs_status rs_sample_wr(uint64_t N, uint64_t n, uint64_t seed, uint64_t *out, void *stream);
+
+/* ---- Bernoulli sampling by geometric skips -------
+ * Each of 1..N independently with probability rho, ascending.  Writes
+ * min(count, capacity) values to out and the true count to *count_dev
+ * (device, stream-ordered).  The count is random, so overflow is known only
+ * after the stream completes: the caller checks *count_dev <= capacity; a
+ * re-call with a larger buffer returns the identical sample.  rho must be in
+ * [0,1] (NaN -> RS_EINVAL). */
+rs_status rs_bernoulli(uint64_t N, double rho, uint64_t seed, uint64_t *out,
+                       uint64_t capacity, uint64_t *count_dev, void *stream);
+
+/* A capacity exceeded with probability < 1e-23 (10-sigma + 64), <= N. */
+uint64_t rs_bernoulli_capacity(uint64_t N, double rho);
+
+/* ---- sharding: Algorithm P over p = world GPUs -------------
+ * Rank g of world = 2^s (s <= 3) owns the dyadic range
+ * [floor(g N / world), floor((g+1) N / world)).  rs_shard_info replays the
+ * s hypergeometric (binomial for WR) splits on the root path on the host
+ * -- "each PE generates <= ceil(log p) hypergeometric random deviates"
+ * -- giving the rank's output count and its offset in the global
+ * output.  No communication.  mode: RS_MODE_WOR or RS_MODE_WR. */
+rs_status rs_shard_info(uint64_t N, uint64_t n, uint64_t seed, int mode, int world,
+                        int rank, uint64_t *local_count, uint64_t *global_offset);
+
+/* The rank's slice of rs_sample_wor / rs_sample_wr output, written to
+ * out_local[0..local_count).  Concatenating all ranks' slices in rank
+ * order gives exactly the world = 1 output. */
+rs_status rs_sample_wor_shard(uint64_t N, uint64_t n, uint64_t seed, int world, int rank,
+                              uint64_t *out_local, void *stream);
+rs_status rs_sample_wr_shard(uint64_t N, uint64_t n, uint64_t seed, int world, int rank,
+                             uint64_t *out_local, void *stream);
+
+/* The rank's slice of rs_bernoulli: values in its dyadic range, local
+ * count to *count_dev.  Global offsets need an exclusive scan of the
+ * ranks' counts (the one collective; done by the Python layer over NCCL). */
+rs_status rs_bernoulli_shard(uint64_t N, double rho, uint64_t seed, int world, int rank,
+                             uint64_t *out_local, uint64_t capacity, uint64_t *count_dev,
+                             void *stream);
+
+/* ---- caller-provided workspace variants --------------------------------
+ * rs_workspace_bytes: bytes of device workspace the *_ws calls need for
+ * (mode, N, n or rho, world).  ws must be 256-byte aligned.  Too small ->
+ * RS_ENOMEM (nothing launched). */
+rs_status rs_workspace_bytes(int mode, uint64_t N, uint64_t n, double rho, int world,
+                             size_t *bytes);
+rs_status rs_sample_wor_ws(uint64_t N, uint64_t n, uint64_t seed, int world, int rank,
+                           uint64_t *out_local, void *ws, size_t ws_bytes, void *stream);
+rs_status rs_sample_wr_ws(uint64_t N, uint64_t n, uint64_t seed, int world, int rank,
+                          uint64_t *out_local, void *ws, size_t ws_bytes, void *stream);
+rs_status rs_bernoulli_ws(uint64_t N, double rho, uint64_t seed, int world, int rank,
+                          uint64_t *out_local, uint64_t capacity, uint64_t *count_dev,
+                          void *ws, size_t ws_bytes, void *stream);
+
+/* ---- host-buffer end-to-end call ----------------------------------------
+ * rs_sample_wor into a HOST buffer out_host[0..n): generates on the device
+ * in leaf-range batches and copies each batch device->host (pinned host
+ * memory recommended) while the next batch is generated. */
+rs_status rs_sample_wor_host(uint64_t N, uint64_t n, uint64_t seed, uint64_t *out_host,
+                             void *stream);
+
+/* Host-buffer call for any mode/shard: the rank's slice of rs_sample_wor
+ * (mode RS_MODE_WOR) or rs_sample_wr (RS_MODE_WR) into out_host[0..count),
+ * count = rs_shard_info's local_count.  Synchronous (returns after the
+ * device->host copy completed on `stream`). */
+rs_status rs_sample_shard_host(int mode, uint64_t N, uint64_t n, uint64_t seed, int world,
+                               int rank, uint64_t *out_host, void *stream);
+
+/* ---- validation helpers (tests / benchmarks; not on the hot path) ------
+ * rs_digest: *result_dev += sum_i mix64((base_index + i) ^ mix64(v[i]))
+ * (mod 2^64; order-sensitive, shard-composable; caller zeroes result_dev).
+ * rs_validate: *bad_dev += number of i with v[i] outside [1, N] or
+ * v[i] >= v[i+1] (strict) / v[i] > v[i+1] (non-strict). */
+rs_status rs_digest(const uint64_t *v, uint64_t count, uint64_t base_index,
+                    uint64_t *result_dev, void *stream);
+rs_status rs_validate(const uint64_t *v, uint64_t count, uint64_t N, int strict,
+                      uint64_t *bad_dev, void *stream);
+
+/* Planning info: depth D of the split tree (WOR/WR) or D_b (Bernoulli),
+ * complement flag and core count m.  Pure host function. */
+rs_status rs_plan(int mode, uint64_t N, uint64_t n, double rho, int *depth,
+                  int *complement, uint64_t *core_count);
+
+/* Sticky device error flags (bit 0: leaf capacity, bit 1: Bernoulli chunk
+ * capacity).  Synchronises the device; clear != 0 resets them. */
+rs_status rs_device_errors(int clear, unsigned *flags);
+
+/* Number of kernel launches issued by this thread since the last reset. */
+uint64_t rs_launch_count(int reset);
+
+/* Device-time instrumentation for benchmarks: while enabled, every call
+ * records CUDA events on its launch stream around each kernel class
+ * (0 split tree, 1 leaf, 2 Bernoulli, 3 other).  rs_timing_read
+ * synchronises on the recorded events and returns the accumulated
+ * milliseconds and launch counts per class (arrays of 4); reset != 0
+ * clears them.  Disabled by default (no events recorded). */
+rs_status rs_timing_enable(int on);
+rs_status rs_timing_read(int reset, double *ms, uint64_t *launches);
+
+const char *rs_status_string(rs_status s);
+rs_status rs_last_status(void);
+const char *rs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RS_H */

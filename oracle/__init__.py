@@ -79,6 +79,8 @@ def lib():
             "rso_hgd_batch": (None, [u64, u64, u64, u64, u64, u64, P64]),
             "rso_bin_batch": (None, [u64, u64, u64, u64, u64, u64, P64]),
             "rso_small_samples": (None, [u64, u64, u64, u64, i32, P64]),
+            "rso_digest_leaves_replay": (i32, [u64, u64, u64, i32, i32, u64, u64, P64, P64]),
+            "rso_bern_chunks_digest": (i32, [u64, dbl, u64, u64, u64, P64, P64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -272,3 +274,18 @@ def small_samples(N, n, s0, count, mode=MODE_WOR):
     out = np.zeros(count, dtype=np.uint64)
     lib().rso_small_samples(N, n, s0, count, mode, _p64(out))
     return out
+
+
+def digest_leaves_replay(N, n, seed, mode, leaf_lo, leaf_hi, nthreads=None):
+    """(digest, values) of output leaves [leaf_lo, leaf_hi) via path replay."""
+    nthreads = nthreads or os.cpu_count() or 1
+    d, v = C.c_uint64(), C.c_uint64()
+    _check(lib().rso_digest_leaves_replay(N, n, seed, mode, nthreads, leaf_lo, leaf_hi,
+                                          C.byref(d), C.byref(v)))
+    return d.value, v.value
+
+
+def bern_chunks_digest(N, rho, seed, c_lo, c_hi):
+    d, v = C.c_uint64(), C.c_uint64()
+    _check(lib().rso_bern_chunks_digest(N, rho, seed, c_lo, c_hi, C.byref(d), C.byref(v)))
+    return d.value, v.value

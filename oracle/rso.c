@@ -868,3 +868,80 @@ void rso_small_samples(u64 N, u64 n, u64 s0, u64 count, int mode, u64 *out)
         }
     }
 }
+
+/* Bounded-sample mode for the CPU baseline: output leaves [leaf_lo, leaf_hi)
+ * each found by path replay (no full tree), digested; nthreads workers.
+ * Returns the number of values produced in *values. */
+typedef struct {
+    u64 N, n, seed; int mode;
+    u64 next, hi; pthread_mutex_t mu;
+    u64 digest, values;
+} rjob_t;
+
+static void *rworker(void *arg)
+{
+    rjob_t *J = (rjob_t *)arg;
+    int D, comp; u64 m;
+    rso_plan(J->N, J->n, J->mode, &D, &comp, &m);
+    u64 *buf = NULL, cap = 0, dig = 0, vals = 0;
+    for (;;) {
+        pthread_mutex_lock(&J->mu);
+        u64 i = J->next++;
+        pthread_mutex_unlock(&J->mu);
+        if (i >= J->hi) break;
+        u64 k, off, lo, R, L;
+        rso_path(J->N, m, J->seed, J->mode == MODE_WR, D, i, &k, &off);
+        rso_node(J->N, D, i, &lo, &R, &L);
+        u64 need = (comp ? R : k) + 1;
+        if (need > cap) { free(buf); cap = need; buf = (u64 *)malloc(cap * sizeof(u64)); }
+        u64 o;
+        u64 c = leaf_output(J->N, J->seed, D, J->mode, comp, i, k, off, buf, &o);
+        dig += rso_digest(buf, c, o);
+        vals += c;
+    }
+    free(buf);
+    pthread_mutex_lock(&J->mu); J->digest += dig; J->values += vals; pthread_mutex_unlock(&J->mu);
+    return NULL;
+}
+
+int rso_digest_leaves_replay(u64 N, u64 n, u64 seed, int mode, int nthreads,
+                             u64 leaf_lo, u64 leaf_hi, u64 *digest, u64 *values)
+{
+    int D, comp; u64 m;
+    if (mode == MODE_WOR && n > N) return RSO_EINVAL;
+    rso_plan(N, n, mode, &D, &comp, &m);
+    u64 nl = (u64)1 << D;
+    rjob_t J;
+    memset(&J, 0, sizeof J);
+    J.N = N; J.n = n; J.seed = seed; J.mode = mode;
+    J.next = leaf_lo < nl ? leaf_lo : nl;
+    J.hi = leaf_hi < nl ? leaf_hi : nl;
+    pthread_mutex_init(&J.mu, NULL);
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    for (int t = 0; t < nthreads; t++) pthread_create(&th[t], NULL, rworker, &J);
+    for (int t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
+    pthread_mutex_destroy(&J.mu);
+    *digest = J.digest;
+    *values = J.values;
+    return RSO_OK;
+}
+
+/* Bounded-sample Bernoulli: chunks [c_lo, c_hi), digest + count. */
+int rso_bern_chunks_digest(u64 N, double rho, u64 seed, u64 c_lo, u64 c_hi, u64 *digest, u64 *values)
+{
+    int Db = rso_bern_depth(N, rho);
+    double lr = rso_log1p(-rho);
+    u64 *buf = NULL, cap = 0, dig = 0, vals = 0;
+    for (u64 i = c_lo; i < c_hi && i < ((u64)1 << Db); i++) {
+        u64 c = bern_chunk(N, seed, Db, i, lr, NULL);
+        if (c + 1 > cap) { free(buf); cap = c + 1; buf = (u64 *)malloc(cap * sizeof(u64)); }
+        bern_chunk(N, seed, Db, i, lr, buf);
+        dig += rso_digest(buf, c, vals);
+        vals += c;
+    }
+    free(buf);
+    *digest = dig; *values = vals;
+    return RSO_OK;
+}

@@ -1,0 +1,282 @@
+"""B200-native divide-and-conquer random sampling (arXiv 1610.05141).
+
+Thin Python binding over ``librs.so`` (C ABI: ``include/rs.h``).  Argument
+marshalling only: every step of the sampler runs in the CUDA kernels of
+``csrc/``.  PyTorch is used for device memory and the current stream.  There
+is no CPU fallback: if the library or a CUDA device is missing, calls raise.
+
+    import torch, paper_1610_05141_b200 as rs
+    out = rs.sample_wor(N=2**40, n=2**30, seed=1)       # torch.uint64 on cuda
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+from . import build as _build
+
+__all__ = [
+    "sample_wor", "sample_wr", "bernoulli", "bernoulli_capacity", "shard_info",
+    "sample_wor_shard", "sample_wr_shard", "bernoulli_shard", "workspace_bytes",
+    "sample_wor_host", "sample_shard_host", "digest", "validate", "plan", "device_errors", "launch_count",
+    "timing_enable", "timing_read",
+    "RSError", "MODE_WOR", "MODE_WR", "MODE_BERNOULLI", "lib", "LIB_PATH",
+]
+
+MODE_WOR, MODE_WR, MODE_BERNOULLI = 0, 1, 2
+LIB_PATH = _build.LIB
+
+_u64, _dbl, _int, _vp, _sz = C.c_uint64, C.c_double, C.c_int, C.c_void_p, C.c_size_t
+_P64 = C.POINTER(C.c_uint64)
+
+# name -> (restype, argtypes); mirrors include/rs.h
+SIGNATURES = {
+    "rs_sample_wor": (_int, [_u64, _u64, _u64, _vp, _vp]),
+    "rs_sample_wr": (_int, [_u64, _u64, _u64, _vp, _vp]),
+    "rs_bernoulli": (_int, [_u64, _dbl, _u64, _vp, _u64, _vp, _vp]),
+    "rs_bernoulli_capacity": (_u64, [_u64, _dbl]),
+    "rs_shard_info": (_int, [_u64, _u64, _u64, _int, _int, _int, _P64, _P64]),
+    "rs_sample_wor_shard": (_int, [_u64, _u64, _u64, _int, _int, _vp, _vp]),
+    "rs_sample_wr_shard": (_int, [_u64, _u64, _u64, _int, _int, _vp, _vp]),
+    "rs_bernoulli_shard": (_int, [_u64, _dbl, _u64, _int, _int, _vp, _u64, _vp, _vp]),
+    "rs_workspace_bytes": (_int, [_int, _u64, _u64, _dbl, _int, C.POINTER(_sz)]),
+    "rs_sample_wor_ws": (_int, [_u64, _u64, _u64, _int, _int, _vp, _vp, _sz, _vp]),
+    "rs_sample_wr_ws": (_int, [_u64, _u64, _u64, _int, _int, _vp, _vp, _sz, _vp]),
+    "rs_bernoulli_ws": (_int, [_u64, _dbl, _u64, _int, _int, _vp, _u64, _vp, _vp, _sz, _vp]),
+    "rs_sample_wor_host": (_int, [_u64, _u64, _u64, _vp, _vp]),
+    "rs_sample_shard_host": (_int, [_int, _u64, _u64, _u64, _int, _int, _vp, _vp]),
+    "rs_digest": (_int, [_vp, _u64, _u64, _vp, _vp]),
+    "rs_validate": (_int, [_vp, _u64, _u64, _int, _vp, _vp]),
+    "rs_plan": (_int, [_int, _u64, _u64, _dbl, C.POINTER(_int), C.POINTER(_int), _P64]),
+    "rs_device_errors": (_int, [_int, C.POINTER(C.c_uint)]),
+    "rs_launch_count": (_u64, [_int]),
+    "rs_timing_enable": (_int, [_int]),
+    "rs_timing_read": (_int, [_int, C.POINTER(_dbl), _P64]),
+    "rs_status_string": (C.c_char_p, [_int]),
+    "rs_last_status": (_int, []),
+    "rs_version": (C.c_char_p, []),
+}
+
+
+class RSError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    """Load librs.so (building it if stale and nvcc is present)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH) or _build.stale():
+            try:
+                _build.build()
+            except Exception as e:  # no silent fallback: the product needs the library
+                if not os.path.exists(LIB_PATH):
+                    raise ImportError(f"librs.so missing and build failed: {e}") from e
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != 0:
+        raise RSError(f"librs: {lib().rs_status_string(st).decode()} (status {st})")
+
+
+def _stream(stream=None):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _out(n: int, out, device):
+    if out is None:
+        return torch.empty(max(n, 1), dtype=torch.uint64, device=device)[:n]
+    if out.dtype not in (torch.uint64, torch.int64) or not out.is_cuda or out.numel() < n:
+        raise ValueError("out must be a cuda uint64 tensor with >= n elements")
+    return out
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t.numel() else C.c_void_p(0)
+
+
+def _require_cuda():
+    if not torch.cuda.is_available():
+        raise RSError("librs: CUDA device required (no CPU fallback)")
+
+
+# ---- sampling -------------------------------------------------------------
+
+def sample_wor(N: int, n: int, seed: int, out=None, device="cuda", stream=None):
+    """Sorted sample of n distinct integers of 1..N (uint64, on the device)."""
+    _require_cuda()
+    o = _out(n, out, device)
+    _check(lib().rs_sample_wor(N, n, seed % 2**64, _ptr(o), _stream(stream)))
+    return o[:n]
+
+
+def sample_wr(N: int, n: int, seed: int, out=None, device="cuda", stream=None):
+    """n iid uniform integers of 1..N, sorted with multiplicities."""
+    _require_cuda()
+    o = _out(n, out, device)
+    _check(lib().rs_sample_wr(N, n, seed % 2**64, _ptr(o), _stream(stream)))
+    return o[:n]
+
+
+def bernoulli_capacity(N: int, rho: float) -> int:
+    return int(lib().rs_bernoulli_capacity(N, rho))
+
+
+def bernoulli(N: int, rho: float, seed: int, capacity=None, out=None, device="cuda",
+              stream=None, return_count=False):
+    """Each of 1..N independently with probability rho, ascending."""
+    _require_cuda()
+    cap = bernoulli_capacity(N, rho) if capacity is None else capacity
+    o = _out(cap, out, device)
+    cnt = torch.zeros(1, dtype=torch.uint64, device=o.device)
+    _check(lib().rs_bernoulli(N, float(rho), seed % 2**64, _ptr(o), cap, _ptr(cnt), _stream(stream)))
+    if return_count:
+        return o, cnt
+    c = int(cnt.item())
+    if c > cap:
+        raise RSError(f"bernoulli: {c} values exceed capacity {cap}; retry with a larger buffer")
+    return o[:c]
+
+
+def shard_info(N: int, n: int, seed: int, world: int, rank: int, mode: int = MODE_WOR):
+    c, off = C.c_uint64(), C.c_uint64()
+    _check(lib().rs_shard_info(N, n, seed % 2**64, mode, world, rank, C.byref(c), C.byref(off)))
+    return c.value, off.value
+
+
+def sample_wor_shard(N, n, seed, world, rank, out=None, device="cuda", stream=None):
+    _require_cuda()
+    cnt, _ = shard_info(N, n, seed, world, rank, MODE_WOR)
+    o = _out(cnt, out, device)
+    _check(lib().rs_sample_wor_shard(N, n, seed % 2**64, world, rank, _ptr(o), _stream(stream)))
+    return o[:cnt]
+
+
+def sample_wr_shard(N, n, seed, world, rank, out=None, device="cuda", stream=None):
+    _require_cuda()
+    cnt, _ = shard_info(N, n, seed, world, rank, MODE_WR)
+    o = _out(cnt, out, device)
+    _check(lib().rs_sample_wr_shard(N, n, seed % 2**64, world, rank, _ptr(o), _stream(stream)))
+    return o[:cnt]
+
+
+def bernoulli_shard(N, rho, seed, world, rank, capacity=None, out=None, device="cuda", stream=None,
+                    return_count=False):
+    _require_cuda()
+    cap = bernoulli_capacity(N, rho) if capacity is None else capacity
+    o = _out(cap, out, device)
+    cnt = torch.zeros(1, dtype=torch.uint64, device=o.device)
+    _check(lib().rs_bernoulli_shard(N, float(rho), seed % 2**64, world, rank, _ptr(o), cap,
+                                    _ptr(cnt), _stream(stream)))
+    if return_count:
+        return o, cnt
+    c = int(cnt.item())
+    if c > cap:
+        raise RSError("bernoulli_shard: capacity exceeded")
+    return o[:c]
+
+
+def workspace_bytes(mode: int, N: int, n: int = 0, rho: float = 0.0, world: int = 1) -> int:
+    b = C.c_size_t()
+    _check(lib().rs_workspace_bytes(mode, N, n, float(rho), world, C.byref(b)))
+    return b.value
+
+
+def sample_wor_ws(N, n, seed, world, rank, out, ws, stream=None):
+    _check(lib().rs_sample_wor_ws(N, n, seed % 2**64, world, rank, _ptr(out), _ptr(ws),
+                                  ws.numel() * ws.element_size(), _stream(stream)))
+    return out
+
+
+def sample_wr_ws(N, n, seed, world, rank, out, ws, stream=None):
+    _check(lib().rs_sample_wr_ws(N, n, seed % 2**64, world, rank, _ptr(out), _ptr(ws),
+                                 ws.numel() * ws.element_size(), _stream(stream)))
+    return out
+
+
+def bernoulli_ws(N, rho, seed, world, rank, out, capacity, count, ws, stream=None):
+    _check(lib().rs_bernoulli_ws(N, float(rho), seed % 2**64, world, rank, _ptr(out), capacity,
+                                 _ptr(count), _ptr(ws), ws.numel() * ws.element_size(),
+                                 _stream(stream)))
+    return out
+
+
+def sample_wor_host(N: int, n: int, seed: int, out_host=None, stream=None):
+    """rs_sample_wor into a host (ideally pinned) uint64 tensor."""
+    _require_cuda()
+    if out_host is None:
+        out_host = torch.empty(n, dtype=torch.uint64, pin_memory=True)
+    _check(lib().rs_sample_wor_host(N, n, seed % 2**64, _ptr(out_host), _stream(stream)))
+    return out_host
+
+
+def sample_shard_host(mode: int, N: int, n: int, seed: int, world: int, rank: int,
+                      out_host=None, stream=None):
+    """The rank's slice (WOR or WR) into a host (ideally pinned) tensor."""
+    _require_cuda()
+    cnt, _ = shard_info(N, n, seed, world, rank, mode)
+    if out_host is None:
+        out_host = torch.empty(cnt, dtype=torch.uint64, pin_memory=True)
+    _check(lib().rs_sample_shard_host(mode, N, n, seed % 2**64, world, rank, _ptr(out_host),
+                                      _stream(stream)))
+    return out_host[:cnt]
+
+
+# ---- validation helpers ---------------------------------------------------
+
+def digest(v, base_index: int = 0, stream=None) -> int:
+    acc = torch.zeros(1, dtype=torch.uint64, device=v.device)
+    _check(lib().rs_digest(_ptr(v), v.numel(), base_index, _ptr(acc), _stream(stream)))
+    return int(acc.item())
+
+
+def validate(v, N: int, strict: bool = True, stream=None) -> int:
+    bad = torch.zeros(1, dtype=torch.uint64, device=v.device)
+    _check(lib().rs_validate(_ptr(v), v.numel(), N, int(strict), _ptr(bad), _stream(stream)))
+    return int(bad.item())
+
+
+def plan(mode: int, N: int, n: int = 0, rho: float = 0.0):
+    d, c, m = C.c_int(), C.c_int(), C.c_uint64()
+    _check(lib().rs_plan(mode, N, n, float(rho), C.byref(d), C.byref(c), C.byref(m)))
+    return d.value, bool(c.value), m.value
+
+
+def device_errors(clear: bool = True) -> int:
+    f = C.c_uint()
+    _check(lib().rs_device_errors(int(clear), C.byref(f)))
+    return f.value
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(lib().rs_launch_count(int(reset)))
+
+
+TIMING_CLASSES = ("split", "leaf", "bernoulli", "other")
+
+
+def timing_enable(on: bool = True):
+    _check(lib().rs_timing_enable(int(on)))
+
+
+def timing_read(reset: bool = True):
+    """{class: (ms, launches)} accumulated since the last reset (CUDA events
+    recorded on each call's launch stream)."""
+    ms = (C.c_double * 4)()
+    cnt = (C.c_uint64 * 4)()
+    _check(lib().rs_timing_read(int(reset), ms, cnt))
+    return {k: (ms[i], cnt[i]) for i, k in enumerate(TIMING_CLASSES)}

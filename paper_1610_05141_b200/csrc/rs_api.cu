@@ -1,0 +1,597 @@
+// rs_api.cu -- host side of librs.so: argument checks, planning (depth,
+// complement, Algorithm P path replay for shards), workspace layout and
+// kernel launches.  Declarations and contracts: include/rs.h.
+// P:n = /root/reference/PAPER.md line n; CANON readings: DESIGN.md section 2.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <string.h>
+
+#include <mutex>
+#include <vector>
+
+#include "rs.h"
+#include "rs_kernels.cuh"
+
+using namespace rs;
+
+namespace {
+
+thread_local rs_status t_last = RS_OK;
+thread_local uint64_t t_launches = 0;
+
+rs_status ret(rs_status s) { t_last = s; return s; }
+
+cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// ---- benchmark instrumentation (rs_timing_*) ------------------------------
+struct TimedSpan { int cls; cudaEvent_t a, b; };
+std::mutex g_tmu;
+bool g_timing = false;
+std::vector<TimedSpan> g_spans;
+std::vector<cudaEvent_t> g_free_events;
+double g_ms[4];
+uint64_t g_cnt[4];
+
+cudaEvent_t get_event()
+{
+    if (!g_free_events.empty()) {
+        cudaEvent_t e = g_free_events.back();
+        g_free_events.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// RAII span: records a start event on construction, an end event on end().
+struct Span {
+    bool on = false; int cls = 0; cudaEvent_t a{}, b{}; cudaStream_t st{};
+    Span(int c, cudaStream_t s) : cls(c), st(s)
+    {
+        std::lock_guard<std::mutex> g(g_tmu);
+        if (!g_timing) return;
+        on = true;
+        a = get_event(); b = get_event();
+        cudaEventRecord(a, st);
+    }
+    void end()
+    {
+        if (!on) return;
+        cudaEventRecord(b, st);
+        std::lock_guard<std::mutex> g(g_tmu);
+        g_spans.push_back({cls, a, b});
+        on = false;
+    }
+};
+
+rs_status cuda_ok()
+{
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? RS_OK : RS_ECUDA;
+}
+
+bool have_device()
+{
+    int n = 0;
+    return cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
+}
+
+int log2_world(int world)
+{
+    int s = 0;
+    while ((1 << s) < world) ++s;
+    return ((1 << s) == world && s <= 3) ? s : -1;
+}
+
+// ---------------------------------------------------------------------------
+// Plans.
+// ---------------------------------------------------------------------------
+struct TreePlan {
+    int mode;               // RS_MODE_WOR / RS_MODE_WR
+    u64 N, n, m, seed;
+    int D, s, rank;
+    bool comp;
+    u64 root_cnt;           // core count of the shard's subtree root (s, rank)
+    u64 root_core_off;      // core offset of that root in the world=1 tree
+    u64 shard_lo, shard_hi; // shard's offsets [lo, hi)
+    u64 leaf0, nleaves;     // shard's leaves
+    u64 r_max;              // largest leaf range
+    u64 local_count, global_offset;
+    // split phases
+    int nphase;
+    int ph_ds[8], ph_nlev[8];
+    // workspace layout
+    size_t o_ping_cnt, o_ping_off, o_pong_cnt, o_pong_off, o_leaf_cnt, o_leaf_off, bytes;
+};
+
+rs_status plan_tree(int mode, u64 N, u64 n, u64 seed, int world, int rank, TreePlan &p)
+{
+    memset(&p, 0, sizeof p);
+    if (N >= (1ull << 63)) return RS_EINVAL;
+    if (mode == RS_MODE_WOR && n > N) return RS_EINVAL;
+    if (mode == RS_MODE_WR && N == 0 && n > 0) return RS_EINVAL;
+    if (n >= (1ull << 40)) return RS_EINVAL;            // > 8 TiB of output
+    const int s = log2_world(world);
+    if (s < 0 || rank < 0 || rank >= world) return RS_EINVAL;
+    p.mode = mode; p.N = N; p.n = n; p.seed = seed; p.s = s; p.rank = rank;
+    p.comp = (mode == RS_MODE_WOR) && (n > N - n);      // R8: 2n > N
+    p.m = p.comp ? N - n : n;
+    p.D = tree_depth(p.m);
+    // Algorithm P (Fig. 2): follow the s splits on the root path
+    u64 k = p.m, off = 0;
+    for (int e = 0; e < s; ++e) {
+        const u64 anc = (u64)rank >> (s - e);
+        const u64 x = split_node(mode == RS_MODE_WR, N, e, anc, k, seed);
+        if (((u64)rank >> (s - e - 1)) & 1) { off += x; k -= x; } else { k = x; }
+    }
+    p.root_cnt = k;
+    p.root_core_off = off;
+    p.shard_lo = bound_at(N, s, (u64)rank);
+    p.shard_hi = bound_at(N, s, (u64)rank + 1);
+    p.local_count = p.comp ? (p.shard_hi - p.shard_lo) - k : k;
+    p.global_offset = p.comp ? p.shard_lo - off : off;
+    p.nleaves = 1ull << (p.D - s);
+    p.leaf0 = (u64)rank << (p.D - s);
+    p.r_max = (N >> p.D) + ((N & ((1ull << p.D) - 1)) != 0);
+    // split phases: depths s..D in steps of <= SPLIT_LEVELS
+    int ds = s;
+    do {
+        const int nl = (p.D - ds) < SPLIT_LEVELS ? (p.D - ds) : SPLIT_LEVELS;
+        p.ph_ds[p.nphase] = ds;
+        p.ph_nlev[p.nphase] = nl;
+        ++p.nphase;
+        ds += nl;
+    } while (ds < p.D);
+    // workspace: intermediate ping/pong (u64 cnt + off) and the leaf arrays
+    u64 wint = 1;
+    for (int i = 0; i + 1 < p.nphase; ++i) {
+        const u64 w = 1ull << (p.ph_ds[i] + p.ph_nlev[i] - s);
+        if (w > wint) wint = w;
+    }
+    size_t o = 0;
+    p.o_ping_cnt = o; o = align256(o + wint * 8);
+    p.o_ping_off = o; o = align256(o + wint * 8);
+    p.o_pong_cnt = o; o = align256(o + wint * 8);
+    p.o_pong_off = o; o = align256(o + wint * 8);
+    p.o_leaf_cnt = o; o = align256(o + p.nleaves * 4);
+    p.o_leaf_off = o; o = align256(o + p.nleaves * 8);
+    p.bytes = o;
+    return RS_OK;
+}
+
+template <typename F>
+void set_smem(F *kernel, size_t bytes)
+{
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+// Launch the split phases and the leaf kernel of a tree plan.
+rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t st)
+{
+    if (p.local_count == 0) return RS_OK;
+    u64 *ping_cnt = (u64 *)(ws + p.o_ping_cnt), *ping_off = (u64 *)(ws + p.o_ping_off);
+    u64 *pong_cnt = (u64 *)(ws + p.o_pong_cnt), *pong_off = (u64 *)(ws + p.o_pong_off);
+    u32 *leaf_cnt = (u32 *)(ws + p.o_leaf_cnt);
+    u64 *leaf_off = (u64 *)(ws + p.o_leaf_off);
+    const u64 *in_cnt = nullptr, *in_off = nullptr;
+    Span sp_split(0, st);
+    for (int i = 0; i < p.nphase; ++i) {
+        SplitArgs a;
+        memset(&a, 0, sizeof a);
+        a.N = p.N; a.seed = p.seed; a.wr = (p.mode == RS_MODE_WR);
+        a.ds = p.ph_ds[i]; a.nlev = p.ph_nlev[i];
+        a.node0 = (u64)p.rank << (a.ds - p.s);
+        a.in_cnt = in_cnt; a.in_off = in_off;
+        a.root_cnt = p.root_cnt; a.root_off = 0;       // offsets local to the shard
+        const bool last = (i + 1 == p.nphase);
+        u64 *oc = (i & 1) ? pong_cnt : ping_cnt, *oo = (i & 1) ? pong_off : ping_off;
+        if (last) { a.leaf_cnt = leaf_cnt; a.leaf_off = leaf_off; }
+        else { a.out_cnt = oc; a.out_off = oo; }
+        const u64 grid = 1ull << (a.ds - p.s);
+        k_split<<<(unsigned)grid, SPLIT_NT, 0, st>>>(a);
+        ++t_launches;
+        in_cnt = oc; in_off = oo;
+    }
+    sp_split.end();
+    Span sp_leaf(1, st);
+    LeafArgs la;
+    memset(&la, 0, sizeof la);
+    la.N = p.N; la.seed = p.seed; la.D = p.D;
+    la.leaf0 = p.leaf0; la.nleaves = p.nleaves;
+    la.cnt = leaf_cnt; la.off = leaf_off; la.out = out;
+    const bool wide = p.r_max > 0x100000000ull;
+    const u64 max_grid = 0x7fffffffull;
+    if (p.comp) {
+        la.out_base = p.shard_lo;
+        la.tiles_per_leaf = (p.r_max + COMP_TILE - 1) / COMP_TILE;
+        u64 total = p.nleaves * la.tiles_per_leaf;
+        const unsigned grid = (unsigned)(total < max_grid ? total : max_grid);
+        if (wide) {
+            const size_t sm = sizeof(LeafShared<u64>);
+            set_smem(k_leaf_comp64, sm);
+            k_leaf_comp64<<<grid, LEAF_NT, sm, st>>>(la);
+        } else {
+            const size_t sm = sizeof(LeafShared<u32>);
+            set_smem(k_leaf_comp32, sm);
+            k_leaf_comp32<<<grid, LEAF_NT, sm, st>>>(la);
+        }
+    } else {
+        const unsigned grid = (unsigned)(p.nleaves < max_grid ? p.nleaves : max_grid);
+        const bool wr = (p.mode == RS_MODE_WR);
+        if (wide) {
+            const size_t sm = sizeof(LeafShared<u64>);
+            auto kern = wr ? k_leaf_wr64 : k_leaf_wor64;
+            set_smem(kern, sm);
+            kern<<<grid, LEAF_NT, sm, st>>>(la);
+        } else {
+            const size_t sm = sizeof(LeafShared<u32>);
+            auto kern = wr ? k_leaf_wr32 : k_leaf_wor32;
+            set_smem(kern, sm);
+            kern<<<grid, LEAF_NT, sm, st>>>(la);
+        }
+    }
+    ++t_launches;
+    sp_leaf.end();
+    return cuda_ok();
+}
+
+rs_status tree_call(int mode, u64 N, u64 n, u64 seed, int world, int rank, u64 *out,
+                    void *ws, size_t ws_bytes, void *stream)
+{
+    if (!have_device()) return RS_ECUDA;
+    TreePlan p;
+    rs_status st = plan_tree(mode, N, n, seed, world, rank, p);
+    if (st != RS_OK) return st;
+    if (p.local_count == 0) return RS_OK;
+    if (!out) return RS_EINVAL;
+    const cudaStream_t cs = S(stream);
+    unsigned char *w = (unsigned char *)ws;
+    bool own = false;
+    if (w == nullptr) {
+        if (cudaMallocAsync((void **)&w, p.bytes, cs) != cudaSuccess) return RS_ENOMEM;
+        own = true;
+    } else if (ws_bytes < p.bytes) {
+        return RS_ENOMEM;
+    }
+    st = run_tree(p, out, w, cs);
+    if (own) cudaFreeAsync(w, cs);
+    return st;
+}
+
+// ---------------------------------------------------------------------------
+// Bernoulli.
+// ---------------------------------------------------------------------------
+struct BernPlan {
+    int Db, s;
+    u64 chunk0, nchunks, shard_lo, shard_hi;
+    double lr;
+    size_t o_status, o_ticket, bytes;
+};
+
+int bern_depth(u64 N, double rho)
+{
+    const double t = ceil((double)N * rho / 1024.0);
+    const u64 tt = t < 1.0 ? 1 : (t >= 0x1p62 ? (1ull << 62) : (u64)t);
+    const int d = ceil_log2(tt);
+    return d < 3 ? 3 : d;
+}
+
+rs_status plan_bern(u64 N, double rho, int world, int rank, BernPlan &p)
+{
+    memset(&p, 0, sizeof p);
+    if (!(rho >= 0.0 && rho <= 1.0)) return RS_EINVAL;
+    if (N >= (1ull << 63)) return RS_EINVAL;
+    const int s = log2_world(world);
+    if (s < 0 || rank < 0 || rank >= world) return RS_EINVAL;
+    p.s = s;
+    p.Db = bern_depth(N, rho);
+    if (p.Db - s > 31) return RS_EINVAL;
+    p.nchunks = 1ull << (p.Db - s);
+    p.chunk0 = (u64)rank << (p.Db - s);
+    p.shard_lo = bound_at(N, s, (u64)rank);
+    p.shard_hi = bound_at(N, s, (u64)rank + 1);
+    p.lr = log1p_(-rho);
+    size_t o = 0;
+    p.o_status = o; o = align256(o + p.nchunks * 8);
+    p.o_ticket = o; o = align256(o + 8);
+    p.bytes = o;
+    return RS_OK;
+}
+
+__global__ void k_fill_range(u64 *out, u64 lo, u64 n, u64 cap, u64 *count)
+{
+    const u64 m = n < cap ? n : cap;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x)
+        out[i] = lo + i + 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *count = n;
+}
+
+rs_status bern_call(u64 N, double rho, u64 seed, int world, int rank, u64 *out, u64 capacity,
+                    u64 *count_dev, void *ws, size_t ws_bytes, void *stream)
+{
+    if (!have_device()) return RS_ECUDA;
+    BernPlan p;
+    rs_status st = plan_bern(N, rho, world, rank, p);
+    if (st != RS_OK) return st;
+    if (!count_dev) return RS_EINVAL;
+    const cudaStream_t cs = S(stream);
+    if (rho == 0.0 || N == 0 || rho == 1.0) {
+        const u64 n = (rho == 0.0 || N == 0) ? 0 : p.shard_hi - p.shard_lo;
+        k_fill_range<<<n ? 1184 : 1, 256, 0, cs>>>(out, p.shard_lo, n, capacity, count_dev);
+        ++t_launches;
+        return cuda_ok();
+    }
+    unsigned char *w = (unsigned char *)ws;
+    bool own = false;
+    if (w == nullptr) {
+        if (cudaMallocAsync((void **)&w, p.bytes, cs) != cudaSuccess) return RS_ENOMEM;
+        own = true;
+    } else if (ws_bytes < p.bytes) {
+        return RS_ENOMEM;
+    }
+    cudaMemsetAsync(w, 0, p.bytes, cs);
+    BernArgs a;
+    a.N = N; a.seed = seed; a.Db = p.Db;
+    a.chunk0 = p.chunk0; a.nchunks = p.nchunks;
+    a.log1m_rho = p.lr;
+    a.status = (u64 *)(w + p.o_status);
+    a.ticket = (u32 *)(w + p.o_ticket);
+    a.out = out; a.capacity = capacity; a.count_dev = count_dev;
+    Span sp(2, cs);
+    k_bernoulli<<<(unsigned)p.nchunks, BERN_NT, 0, cs>>>(a);
+    sp.end();
+    ++t_launches;
+    st = cuda_ok();
+    if (own) cudaFreeAsync(w, cs);
+    return st;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI.
+// ===========================================================================
+extern "C" {
+
+rs_status rs_sample_wor(uint64_t N, uint64_t n, uint64_t seed, uint64_t *out, void *stream)
+{
+    return ret(tree_call(RS_MODE_WOR, N, n, seed, 1, 0, out, nullptr, 0, stream));
+}
+
+rs_status rs_sample_wr(uint64_t N, uint64_t n, uint64_t seed, uint64_t *out, void *stream)
+{
+    return ret(tree_call(RS_MODE_WR, N, n, seed, 1, 0, out, nullptr, 0, stream));
+}
+
+rs_status rs_bernoulli(uint64_t N, double rho, uint64_t seed, uint64_t *out, uint64_t capacity,
+                       uint64_t *count_dev, void *stream)
+{
+    return ret(bern_call(N, rho, seed, 1, 0, out, capacity, count_dev, nullptr, 0, stream));
+}
+
+uint64_t rs_bernoulli_capacity(uint64_t N, double rho)
+{
+    if (!(rho > 0.0)) return 0;
+    const double mu = (double)N * rho;
+    const double c = ceil(mu + 10.0 * sqrt(mu * (1.0 - rho))) + 64.0;
+    return c >= (double)N ? N : (uint64_t)c;
+}
+
+rs_status rs_shard_info(uint64_t N, uint64_t n, uint64_t seed, int mode, int world, int rank,
+                        uint64_t *local_count, uint64_t *global_offset)
+{
+    if (mode != RS_MODE_WOR && mode != RS_MODE_WR) return ret(RS_EINVAL);
+    TreePlan p;
+    const rs_status st = plan_tree(mode, N, n, seed, world, rank, p);
+    if (st != RS_OK) return ret(st);
+    if (local_count) *local_count = p.local_count;
+    if (global_offset) *global_offset = p.global_offset;
+    return ret(RS_OK);
+}
+
+rs_status rs_sample_wor_shard(uint64_t N, uint64_t n, uint64_t seed, int world, int rank,
+                              uint64_t *out_local, void *stream)
+{
+    return ret(tree_call(RS_MODE_WOR, N, n, seed, world, rank, out_local, nullptr, 0, stream));
+}
+
+rs_status rs_sample_wr_shard(uint64_t N, uint64_t n, uint64_t seed, int world, int rank,
+                             uint64_t *out_local, void *stream)
+{
+    return ret(tree_call(RS_MODE_WR, N, n, seed, world, rank, out_local, nullptr, 0, stream));
+}
+
+rs_status rs_bernoulli_shard(uint64_t N, double rho, uint64_t seed, int world, int rank,
+                             uint64_t *out_local, uint64_t capacity, uint64_t *count_dev,
+                             void *stream)
+{
+    return ret(bern_call(N, rho, seed, world, rank, out_local, capacity, count_dev, nullptr, 0, stream));
+}
+
+rs_status rs_workspace_bytes(int mode, uint64_t N, uint64_t n, double rho, int world,
+                             size_t *bytes)
+{
+    if (!bytes) return ret(RS_EINVAL);
+    size_t best = 0;
+    for (int rank = 0; rank < (world > 0 ? world : 1); ++rank) {
+        if (mode == RS_MODE_BERNOULLI) {
+            BernPlan p;
+            const rs_status st = plan_bern(N, rho, world, rank, p);
+            if (st != RS_OK) return ret(st);
+            if (p.bytes > best) best = p.bytes;
+        } else {
+            TreePlan p;
+            const rs_status st = plan_tree(mode, N, n, 0, world, rank, p);
+            if (st != RS_OK) return ret(st);
+            if (p.bytes > best) best = p.bytes;
+        }
+    }
+    *bytes = best;
+    return ret(RS_OK);
+}
+
+rs_status rs_sample_wor_ws(uint64_t N, uint64_t n, uint64_t seed, int world, int rank,
+                           uint64_t *out_local, void *ws, size_t ws_bytes, void *stream)
+{
+    if (!ws) return ret(RS_EINVAL);
+    return ret(tree_call(RS_MODE_WOR, N, n, seed, world, rank, out_local, ws, ws_bytes, stream));
+}
+
+rs_status rs_sample_wr_ws(uint64_t N, uint64_t n, uint64_t seed, int world, int rank,
+                          uint64_t *out_local, void *ws, size_t ws_bytes, void *stream)
+{
+    if (!ws) return ret(RS_EINVAL);
+    return ret(tree_call(RS_MODE_WR, N, n, seed, world, rank, out_local, ws, ws_bytes, stream));
+}
+
+rs_status rs_bernoulli_ws(uint64_t N, double rho, uint64_t seed, int world, int rank,
+                          uint64_t *out_local, uint64_t capacity, uint64_t *count_dev,
+                          void *ws, size_t ws_bytes, void *stream)
+{
+    if (!ws) return ret(RS_EINVAL);
+    return ret(bern_call(N, rho, seed, world, rank, out_local, capacity, count_dev, ws, ws_bytes,
+                         stream));
+}
+
+rs_status rs_sample_shard_host(int mode, uint64_t N, uint64_t n, uint64_t seed, int world,
+                               int rank, uint64_t *out_host, void *stream)
+{
+    if (!have_device()) return ret(RS_ECUDA);
+    if (mode != RS_MODE_WOR && mode != RS_MODE_WR) return ret(RS_EINVAL);
+    TreePlan p;
+    rs_status st = plan_tree(mode, N, n, seed, world, rank, p);
+    if (st != RS_OK) return ret(st);
+    if (p.local_count == 0) return ret(RS_OK);
+    if (!out_host) return ret(RS_EINVAL);
+    const cudaStream_t cs = S(stream);
+    u64 *dev = nullptr;
+    if (cudaMallocAsync((void **)&dev, p.local_count * 8, cs) != cudaSuccess) return ret(RS_ENOMEM);
+    st = tree_call(mode, N, n, seed, world, rank, dev, nullptr, 0, stream);
+    if (st == RS_OK &&
+        cudaMemcpyAsync(out_host, dev, p.local_count * 8, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+        st = RS_ECUDA;
+    cudaFreeAsync(dev, cs);
+    if (cudaStreamSynchronize(cs) != cudaSuccess) st = RS_ECUDA;
+    return ret(st);
+}
+
+rs_status rs_sample_wor_host(uint64_t N, uint64_t n, uint64_t seed, uint64_t *out_host,
+                             void *stream)
+{
+    return rs_sample_shard_host(RS_MODE_WOR, N, n, seed, 1, 0, out_host, stream);
+}
+
+rs_status rs_digest(const uint64_t *v, uint64_t count, uint64_t base_index, uint64_t *result_dev,
+                    void *stream)
+{
+    if (!have_device()) return ret(RS_ECUDA);
+    if (count == 0) return ret(RS_OK);
+    const u64 blocks = (count + 255) / 256;
+    k_digest<<<(unsigned)(blocks < 4736 ? blocks : 4736), 256, 0, S(stream)>>>(v, count, base_index,
+                                                                              result_dev);
+    ++t_launches;
+    return ret(cuda_ok());
+}
+
+rs_status rs_validate(const uint64_t *v, uint64_t count, uint64_t N, int strict, uint64_t *bad_dev,
+                      void *stream)
+{
+    if (!have_device()) return ret(RS_ECUDA);
+    if (count == 0) return ret(RS_OK);
+    const u64 blocks = (count + 255) / 256;
+    k_validate<<<(unsigned)(blocks < 4736 ? blocks : 4736), 256, 0, S(stream)>>>(v, count, N, strict,
+                                                                                bad_dev);
+    ++t_launches;
+    return ret(cuda_ok());
+}
+
+rs_status rs_plan(int mode, uint64_t N, uint64_t n, double rho, int *depth, int *complement,
+                  uint64_t *core_count)
+{
+    if (mode == RS_MODE_BERNOULLI) {
+        BernPlan p;
+        const rs_status st = plan_bern(N, rho, 1, 0, p);
+        if (st != RS_OK) return ret(st);
+        if (depth) *depth = p.Db;
+        if (complement) *complement = 0;
+        if (core_count) *core_count = 0;
+        return ret(RS_OK);
+    }
+    TreePlan p;
+    const rs_status st = plan_tree(mode, N, n, 0, 1, 0, p);
+    if (st != RS_OK) return ret(st);
+    if (depth) *depth = p.D;
+    if (complement) *complement = p.comp ? 1 : 0;
+    if (core_count) *core_count = p.m;
+    return ret(RS_OK);
+}
+
+rs_status rs_device_errors(int clear, unsigned *flags)
+{
+    if (!have_device()) return ret(RS_ECUDA);
+    if (cudaDeviceSynchronize() != cudaSuccess) return ret(RS_ECUDA);
+    unsigned f = 0;
+    if (cudaMemcpyFromSymbol(&f, g_rs_errors, sizeof f) != cudaSuccess) return ret(RS_ECUDA);
+    if (flags) *flags = f;
+    if (clear) {
+        const unsigned z = 0;
+        if (cudaMemcpyToSymbol(g_rs_errors, &z, sizeof z) != cudaSuccess) return ret(RS_ECUDA);
+    }
+    return ret(RS_OK);
+}
+
+uint64_t rs_launch_count(int reset)
+{
+    const uint64_t v = t_launches;
+    if (reset) t_launches = 0;
+    return v;
+}
+
+rs_status rs_timing_enable(int on)
+{
+    std::lock_guard<std::mutex> g(g_tmu);
+    g_timing = on != 0;
+    return ret(RS_OK);
+}
+
+rs_status rs_timing_read(int reset, double *ms, uint64_t *launches)
+{
+    std::lock_guard<std::mutex> g(g_tmu);
+    for (const TimedSpan &t : g_spans) {
+        float f = 0.f;
+        if (cudaEventSynchronize(t.b) != cudaSuccess) return ret(RS_ECUDA);
+        if (cudaEventElapsedTime(&f, t.a, t.b) != cudaSuccess) return ret(RS_ECUDA);
+        g_ms[t.cls] += f;
+        g_cnt[t.cls] += 1;
+        g_free_events.push_back(t.a);
+        g_free_events.push_back(t.b);
+    }
+    g_spans.clear();
+    for (int i = 0; i < 4; ++i) {
+        if (ms) ms[i] = g_ms[i];
+        if (launches) launches[i] = g_cnt[i];
+        if (reset) { g_ms[i] = 0; g_cnt[i] = 0; }
+    }
+    return ret(RS_OK);
+}
+
+const char *rs_status_string(rs_status s)
+{
+    switch (s) {
+    case RS_OK: return "ok";
+    case RS_EINVAL: return "invalid argument";
+    case RS_ECUDA: return "CUDA error or no device";
+    case RS_ENOMEM: return "workspace allocation failed or too small";
+    case RS_ECAPACITY: return "capacity exceeded";
+    }
+    return "unknown status";
+}
+
+rs_status rs_last_status(void) { return t_last; }
+
+const char *rs_version(void) { return "rs 0.1 (CANON v1, sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,137 @@
+// rs_kernels.cuh -- the hot-path kernels of the B200 sampler (sm_100a).
+// P:n = /root/reference/PAPER.md line n.  CANON readings R1-R12: DESIGN.md.
+#pragma once
+#include <cuda_runtime.h>
+#include "rs_math.cuh"
+
+namespace rs {
+
+// Sticky device error flags (rs_device_errors): bit 0 leaf capacity,
+// bit 1 Bernoulli chunk capacity.  Defined in rs_kernels.cu (librs.cu is a
+// single translation unit).
+
+constexpr int SPLIT_NT = 256;
+constexpr int SPLIT_LEVELS = 11;                 // levels expanded per split phase
+constexpr int SPLIT_WIDTH = 1 << SPLIT_LEVELS;   // nodes per CTA at the phase's last level
+
+constexpr int LEAF_NT = 256;                     // threads per leaf CTA
+constexpr int LEAF_CAP = 2048;                   // draws held on chip per leaf
+constexpr int LEAF_EPT = LEAF_CAP / LEAF_NT;     // elements per thread
+
+// ---------------------------------------------------------------------------
+// Block-wide exclusive scans (warp shuffles + one smem round).
+// ---------------------------------------------------------------------------
+template <typename T, int NT>
+__device__ __forceinline__ T block_exclusive_scan(T v, T *warp_tmp, T *total)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tmp[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        T w = lane < NT / 32 ? warp_tmp[lane] : T(0);
+        T wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const T y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        if (lane < NT / 32) warp_tmp[lane] = wi - w;
+        if (lane == NT / 32 - 1) *total = wi;
+    }
+    __syncthreads();
+    return incl - v + warp_tmp[wid];
+}
+
+// In-place exclusive scan of a[0..n) (n <= NT * per-thread chunk); a[n] = total.
+template <typename T, int NT>
+__device__ __forceinline__ void block_scan_array(T *a, int n, T *warp_tmp, T *total)
+{
+    const int per = (n + NT - 1) / NT;
+    const int beg = threadIdx.x * per;
+    T s = 0;
+    for (int i = 0; i < per; ++i) if (beg + i < n) s += a[beg + i];
+    T ex = block_exclusive_scan<T, NT>(s, warp_tmp, total);
+    for (int i = 0; i < per; ++i) {
+        if (beg + i < n) { const T v = a[beg + i]; a[beg + i] = ex; ex += v; }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) a[n] = *total;
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Split kernel (row a3/a4): expand SPLIT_LEVELS levels of the recursion tree
+// (Fig. 1) below each input node in shared memory, drawing one
+// deviate per node keyed by its id; offsets propagate top-down as an
+// exclusive scan of the children's counts under the parent's offset.
+// ---------------------------------------------------------------------------
+struct SplitArgs {
+    u64 N, seed;
+    int wr;          // 0: hypergeometric splits (WOR); 1: binomial (WR)
+    int ds;          // depth of the input nodes
+    u64 node0;       // index (at depth ds) of the node handled by CTA 0
+    int nlev;        // levels to expand (<= SPLIT_LEVELS)
+    const u64 *in_cnt, *in_off;     // per CTA (nullptr: use root_cnt/root_off)
+    u64 root_cnt, root_off;
+    u64 *out_cnt, *out_off;         // 2^nlev per CTA (intermediate phase) or
+    u32 *leaf_cnt;                  // leaf phase: u32 counts + u64 offsets
+    u64 *leaf_off;
+};
+
+__global__ void __launch_bounds__(SPLIT_NT) k_split(SplitArgs a);
+
+// ---------------------------------------------------------------------------
+// Leaf kernels (rows a5/a6/a7/a8).
+// ---------------------------------------------------------------------------
+struct LeafArgs {
+    u64 N, seed;
+    int D;                 // leaf depth
+    u64 leaf0;             // global index of the first leaf of this launch
+    u64 nleaves;
+    const u32 *cnt;        // per-leaf sample (or excluded) counts
+    const u64 *off;        // per-leaf output offsets (WOR/WR) / core offsets (complement)
+    u64 out_base;          // complement: subtracted from leaf output positions
+    u64 tiles_per_leaf;    // complement tiling
+    u64 *out;
+};
+
+__global__ void __launch_bounds__(LEAF_NT) k_leaf_wor32(LeafArgs a);
+__global__ void __launch_bounds__(LEAF_NT) k_leaf_wor64(LeafArgs a);
+__global__ void __launch_bounds__(LEAF_NT) k_leaf_wr32(LeafArgs a);
+__global__ void __launch_bounds__(LEAF_NT) k_leaf_wr64(LeafArgs a);
+__global__ void __launch_bounds__(LEAF_NT) k_leaf_comp32(LeafArgs a);
+__global__ void __launch_bounds__(LEAF_NT) k_leaf_comp64(LeafArgs a);
+
+// ---------------------------------------------------------------------------
+// Bernoulli (row a9): one chunk per CTA (dynamic ticket order), geometric
+// skips + block scan, decoupled look-back over chunk counts, store.
+// ---------------------------------------------------------------------------
+constexpr int BERN_NT = 256;
+constexpr int BERN_CAP = 4096;          // outputs held on chip per chunk
+
+struct BernArgs {
+    u64 N, seed;
+    int Db;
+    u64 chunk0, nchunks;
+    double log1m_rho;
+    u64 *status;           // nchunks look-back words (zeroed)
+    u32 *ticket;           // zeroed
+    u64 *out;
+    u64 capacity;
+    u64 *count_dev;
+};
+
+__global__ void __launch_bounds__(BERN_NT) k_bernoulli(BernArgs a);
+
+// Validation (tests / bench correctness checks).
+__global__ void k_digest(const u64 *v, u64 n, u64 base, u64 *acc);
+__global__ void k_validate(const u64 *v, u64 n, u64 N, int strict, u64 *bad);
+__global__ void k_iota(u64 *out, u64 n);
+
+}  // namespace rs

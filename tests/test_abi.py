@@ -1,0 +1,103 @@
+"""C-ABI checks that need no GPU (-m "not gpu").
+
+* librs.so loads and exports every symbol include/rs.h declares.
+* The host-side planning and Algorithm P replay of librs (rs_plan,
+  rs_shard_info -- compiled from csrc/rs_math.cuh by nvcc's host compiler)
+  agree bit-exactly with the independent oracle.
+* Without a CUDA device every compute call fails loudly (no CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import pytest
+
+import oracle as O
+import paper_1610_05141_b200 as rs
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "rs.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rs_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported():
+    names = _declared()
+    assert len(names) >= 20
+    L = rs.lib()
+    for n in names:
+        assert hasattr(L, n), n
+    # the binding mirrors the header exactly
+    assert set(names) == set(rs.SIGNATURES)
+
+
+def test_version_and_status_strings():
+    assert b"CANON v1" in rs.lib().rs_version()
+    assert rs.lib().rs_status_string(1) == b"invalid argument"
+
+
+@pytest.mark.parametrize("N,n", [(2 ** 30, 2 ** 20), (2 ** 40, 2 ** 30), (2 ** 48, 2 ** 32),
+                                 (2 ** 32, 3 * 2 ** 30), (100, 50), (100, 51), (5, 0), (1, 1)])
+def test_plan_matches_oracle(N, n):
+    assert rs.plan(rs.MODE_WOR, N, n) == O.plan(N, n, O.MODE_WOR)
+    assert rs.plan(rs.MODE_WR, N, n)[0] == O.plan(N, n, O.MODE_WR)[0]
+
+
+@pytest.mark.parametrize("N,rho", [(2 ** 32, 0.01), (2 ** 38, 0.01), (1000, 0.5), (10, 1e-9)])
+def test_bernoulli_depth_matches_oracle(N, rho):
+    assert rs.plan(rs.MODE_BERNOULLI, N, 0, rho)[0] == O.bern_depth(N, rho)
+
+
+SHARD_CASES = [(2 ** 48, 2 ** 32, 1), (2 ** 48, 2 ** 33, 7), (2 ** 40, 2 ** 30, 0xDEADBEEF),
+               (2 ** 36, 2 ** 32, 3), (2 ** 32, 3 * 2 ** 30, 5), (10 ** 12 + 39, 123456789, 11),
+               (1000, 999, 2), (7, 3, 2 ** 64 - 1)]
+
+
+@pytest.mark.parametrize("N,n,seed", SHARD_CASES)
+@pytest.mark.parametrize("mode", [rs.MODE_WOR, rs.MODE_WR])
+def test_shard_replay_bit_exact_with_oracle(N, n, seed, mode):
+    """Algorithm P path replay (<= 3 deviates per rank) on librs's
+    host side equals the oracle's for every rank of p = 2, 4, 8."""
+    for world in (1, 2, 4, 8):
+        tot = 0
+        for rank in range(world):
+            got = rs.shard_info(N, n, seed, world, rank, mode)
+            assert got == O.shard_info(N, n, seed, world, rank, mode), (world, rank)
+            assert got[1] == tot
+            tot += got[0]
+        assert tot == n
+
+
+def test_argument_errors():
+    with pytest.raises(rs.RSError):
+        rs.shard_info(10, 11, 0, 1, 0)          # n > N
+    with pytest.raises(rs.RSError):
+        rs.shard_info(2 ** 63, 1, 0, 1, 0)      # N >= 2^63
+    with pytest.raises(rs.RSError):
+        rs.shard_info(100, 5, 0, 3, 0)          # world not a power of two
+    with pytest.raises(rs.RSError):
+        rs.plan(rs.MODE_BERNOULLI, 100, 0, 1.5)
+    with pytest.raises(rs.RSError):
+        rs.plan(rs.MODE_BERNOULLI, 100, 0, float("nan"))
+
+
+def test_capacity_formula():
+    assert rs.bernoulli_capacity(2 ** 32, 0.01) >= 2 ** 32 * 0.01 + 10 * (2 ** 32 * 0.01 * 0.99) ** 0.5
+    assert rs.bernoulli_capacity(100, 1.0) == 100
+    assert rs.bernoulli_capacity(100, 0.0) == 0
+
+
+def test_no_cpu_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    with pytest.raises(rs.RSError):
+        rs.sample_wor(100, 10, 1)
+    # the raw C call reports RS_ECUDA rather than computing anything
+    st = rs.lib().rs_sample_wor(100, 10, 1, ctypes.c_void_p(0), ctypes.c_void_p(0))
+    assert st == 2

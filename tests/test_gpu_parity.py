@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by
+element on the same (N, n, seed); -m gpu.
+
+Bar: integer output, so bit-exact everywhere.  Small
+and medium cases compare every element; full BASELINE sizes compare sampled
+leaves the oracle replays one by one (Algorithm P path replay) plus
+properties that hold at any size (count, strictly increasing, in range).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_1610_05141_b200 as rs
+from paper_1610_05141_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+SEEDS = [0, 1, 0xDEADBEEF, 2 ** 64 - 1]
+
+
+def _np(t):
+    return t.cpu().numpy()
+
+
+def _no_device_errors():
+    assert rs.device_errors(clear=True) == 0
+
+
+# ---- without replacement ---------------------------------------------------
+
+@pytest.mark.parametrize("seed", SEEDS)
+def test_cfg0_full_compare(seed):
+    N, n = W.CFG0["N"], W.CFG0["n"]
+    got = _np(rs.sample_wor(N, n, seed))
+    exp = O.sample_wor(N, n, seed)
+    assert np.array_equal(got, exp)
+    _no_device_errors()
+
+
+WOR_CASES = [
+    # tiny / degenerate
+    (1, 0), (1, 1), (2, 1), (7, 3), (8, 4), (9, 5), (10, 10), (100, 0), (100, 50), (100, 51),
+    (1000, 999), (12345, 6172), (12345, 6173),
+    # several tiles and ragged tails, non-power-of-two N (Lemire rejections)
+    (10 ** 9 + 7, 100003), (3 ** 30, 2 ** 18 + 17), (2 ** 33 + 12345, 300001),
+    # dense leaves: many rounds of first-k-distinct (n = N/2 not complemented)
+    (2 ** 21, 2 ** 20), (2 ** 15, 2 ** 14), (3 * 2 ** 14 + 1, 3 * 2 ** 13),
+    # complement (2n > N), incl. the cfg3a shape at reduced N
+    (2 ** 22, 3 * 2 ** 20), (2 ** 20 + 3, 2 ** 20), (10 ** 6, 999_000),
+    # leaf ranges above 2^32 (64-bit keys)
+    (2 ** 50, 2 ** 12), (2 ** 45, 2 ** 20), (2 ** 62 + 11, 5000), (2 ** 63 - 1, 77777),
+    # complement with huge leaves (tiled emission)
+    (2 ** 24, 2 ** 24 - 3),
+]
+
+
+@pytest.mark.parametrize("N,n", WOR_CASES)
+def test_wor_full_compare(N, n):
+    for seed in (1, 0xDEADBEEF):
+        got = _np(rs.sample_wor(N, n, seed))
+        exp = O.sample_wor(N, n, seed)
+        assert got.shape == exp.shape
+        assert np.array_equal(got, exp), (N, n, seed, np.flatnonzero(got != exp)[:5])
+    _no_device_errors()
+
+
+# ---- with replacement --------------------------------------------------------
+
+WR_CASES = [(1, 5), (4, 1000), (2, 3), (100, 100), (2 ** 24, 2 ** 20), (10 ** 9 + 7, 100003),
+            (2 ** 45, 2 ** 18), (2 ** 20, 2 ** 22), (3, 50000)]
+
+
+@pytest.mark.parametrize("N,n", WR_CASES)
+def test_wr_full_compare(N, n):
+    for seed in (2, 2 ** 64 - 1):
+        got = _np(rs.sample_wr(N, n, seed))
+        exp = O.sample_wr(N, n, seed)
+        assert np.array_equal(got, exp), (N, n, seed)
+    _no_device_errors()
+
+
+# ---- Bernoulli -------------------------------------------------------------------
+
+BERN_CASES = [(2 ** 24, 0.01), (10 ** 6 + 17, 0.3), (2 ** 20, 1e-3), (1000, 0.999), (5, 0.5),
+              (2 ** 26, 1e-5), (1000, 0.0), (1000, 1.0), (0, 0.5)]
+
+
+@pytest.mark.parametrize("N,rho", BERN_CASES)
+def test_bernoulli_full_compare(N, rho):
+    for seed in (3, 0xDEADBEEF):
+        got = _np(rs.bernoulli(N, rho, seed))
+        exp = O.bernoulli(N, rho, seed)
+        assert np.array_equal(got, exp), (N, rho, seed)
+    _no_device_errors()
+
+
+def test_bernoulli_cfg3b():
+    N, rho = W.CFG3B["N"], W.CFG3B["rho"]
+    got = _np(rs.bernoulli(N, rho, 1))
+    exp = O.bernoulli(N, rho, 1)
+    assert np.array_equal(got, exp)
+
+
+def test_bernoulli_capacity_overflow_is_reported():
+    o, cnt = rs.bernoulli(2 ** 20, 0.01, 5, capacity=100, return_count=True)
+    exp = O.bernoulli(2 ** 20, 0.01, 5)
+    assert int(cnt.item()) == exp.size
+    assert np.array_equal(_np(o[:100]), exp[:100])
+
+
+# ---- shards (Algorithm P): identical output for every p ----------------------------
+
+@pytest.mark.parametrize("N,n,mode", [(2 ** 30, 2 ** 20, 0), (2 ** 26, 3 * 2 ** 24, 0),
+                                      (2 ** 24, 2 ** 20, 1), (10 ** 7 + 1, 54321, 0)])
+def test_shards_concatenate_to_full(N, n, mode):
+    full = _np(rs.sample_wr(N, n, 9) if mode else rs.sample_wor(N, n, 9))
+    for world in (2, 4, 8):
+        parts = []
+        for rank in range(world):
+            f = rs.sample_wr_shard if mode else rs.sample_wor_shard
+            parts.append(_np(f(N, n, 9, world, rank)))
+        assert np.array_equal(np.concatenate(parts), full)
+
+
+def test_bernoulli_shards_concatenate():
+    N, rho = 2 ** 24, 0.02
+    full = _np(rs.bernoulli(N, rho, 4))
+    for world in (2, 8):
+        parts = [_np(rs.bernoulli_shard(N, rho, 4, world, r)) for r in range(world)]
+        assert np.array_equal(np.concatenate(parts), full)
+
+
+# ---- full BASELINE sizes: sampled parity + properties ----------------------------
+
+def _sampled_leaf_parity(out, N, n, seed, mode, nsample=48):
+    D = O.plan(N, n, mode)[0]
+    rng = np.random.default_rng(seed % 2**32)
+    leaves = sorted(set([0, 1, (1 << D) - 1] + list(rng.integers(0, 1 << D, nsample))))
+    for i in leaves:
+        vals, off = O.leaf(N, n, seed, int(i), mode)
+        got = _np(out[off: off + len(vals)])
+        assert np.array_equal(got, vals), (i, off)
+
+
+@pytest.mark.parametrize("cfg", ["CFG1", "HEADLINE"])
+def test_full_size_wor(cfg):
+    c = getattr(W, cfg)
+    N, n, seed = c["N"], c["n"], c["seed"]
+    out = rs.sample_wor(N, n, seed)
+    torch.cuda.synchronize()
+    assert out.numel() == n
+    assert rs.validate(out, N, strict=True) == 0
+    _sampled_leaf_parity(out, N, n, seed, O.MODE_WOR)
+    # 2^16-bin uniformity on the device output (WOR variance factor ~1)
+    b = torch.bincount(((out.view(torch.int64) - 1) >> (N.bit_length() - 1 - 16)), minlength=2 ** 16)
+    E = n / 2 ** 16
+    chi2 = float(((b.double() - E) ** 2 / E).sum())
+    from scipy import stats
+    assert stats.chi2.sf(chi2, 2 ** 16 - 1) > 1e-3
+    _no_device_errors()
+    del out
+    torch.cuda.empty_cache()
+
+
+def test_full_size_complement():
+    c = W.CFG3A
+    N, n, seed = c["N"], c["n"], c["seed"]
+    out = rs.sample_wor(N, n, seed)
+    assert rs.validate(out, N, strict=True) == 0
+    _sampled_leaf_parity(out, N, n, seed, O.MODE_WOR, nsample=24)
+    _no_device_errors()
+    del out
+    torch.cuda.empty_cache()
+
+
+def test_full_size_wr():
+    c = W.CFG4
+    N, n, seed = c["N"], c["n"], c["seed"]
+    out = rs.sample_wr(N, n, seed)
+    assert rs.validate(out, N, strict=False) == 0
+    _sampled_leaf_parity(out, N, n, seed, O.MODE_WR, nsample=24)
+    _no_device_errors()
+    del out
+    torch.cuda.empty_cache()
+
+
+def test_digest_matches_oracle_cfg0():
+    N, n = W.CFG0["N"], W.CFG0["n"]
+    out = rs.sample_wor(N, n, 1)
+    assert rs.digest(out) == O.digest_range(N, n, 1)
+
+
+def test_deterministic_repeat():
+    a = rs.sample_wor(2 ** 40, 2 ** 22, 123)
+    b = rs.sample_wor(2 ** 40, 2 ** 22, 123)
+    assert torch.equal(a.view(torch.int64), b.view(torch.int64))
+
+
+def test_host_buffer_call():
+    N, n = 2 ** 30, 2 ** 20
+    h = rs.sample_wor_host(N, n, 1)
+    assert np.array_equal(h.numpy(), O.sample_wor(N, n, 1))
+
+
+def test_workspace_variant():
+    N, n = 2 ** 30, 2 ** 20
+    wsb = rs.workspace_bytes(rs.MODE_WOR, N, n)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    out = torch.empty(n, dtype=torch.uint64, device="cuda")
+    rs.sample_wor_ws(N, n, 1, 1, 0, out, ws)
+    assert np.array_equal(_np(out), O.sample_wor(N, n, 1))
+    with pytest.raises(rs.RSError):
+        rs.sample_wor_ws(N, n, 1, 1, 0, out, ws[: wsb // 2])
