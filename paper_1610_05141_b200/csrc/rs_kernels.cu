@@ -281,6 +281,49 @@ __device__ __forceinline__ LeafGeom leaf_geom(const LeafArgs &a, u64 L)
     return g;
 }
 
+// WR leaves with more draws than the on-chip capacity.  This happens only
+// when N < 2^D (leaf ranges r <= 1) -- e.g. n >> N -- or with probability
+// < 1e-100 otherwise.  r == 1: k copies of lo+1 (the draws cannot change
+// the value).  r <= WR_HIST: histogram of all k draws (smem atomics), scan,
+// emit runs by binary search over the run starts.  Else: capacity flag.
+constexpr u32 WR_HIST = 2 * LEAF_CAP - 1;
+
+template <typename K>
+__device__ void wr_big_leaf(LeafShared<K> &sh, const Stream &st, u64 lo, u64 r, u32 k, u64 *dst)
+{
+    const u64 base = lo + 1;
+    if (r == 1) {
+        for (u32 i = threadIdx.x; i < k; i += LEAF_NT) dst[i] = base;
+        return;
+    }
+    if (r > WR_HIST) {
+        if (threadIdx.x == 0) atomicOr(&g_rs_errors, 1u);
+        return;
+    }
+    u32 *hist = reinterpret_cast<u32 *>(sh.keys);        // WR_HIST + 1 counters fit keys+stage
+    for (u32 i = threadIdx.x; i <= (u32)r; i += LEAF_NT) hist[i] = 0;
+    __syncthreads();
+    const Drawer<K> dr(st, r);
+    constexpr int EPB = Drawer<K>::EPB;
+    const u64 nblk = ((u64)k + EPB - 1) / EPB;
+    for (u64 q = threadIdx.x; q < nblk; q += LEAF_NT) {
+        K v[EPB];
+        dr.block(q, v);
+        for (int w = 0; w < EPB; ++w)
+            if (q * EPB + w < k) atomicAdd(&hist[(u32)v[w]], 1u);
+    }
+    __syncthreads();
+    block_scan_array<u32, LEAF_NT>(hist, (int)r, sh.wtmp, &sh.tot);
+    for (u32 t = threadIdx.x; t < k; t += LEAF_NT) {
+        u32 a = 0, b = (u32)r;                          // last v with hist[v] <= t
+        while (b - a > 1) {
+            const u32 mid = (a + b) >> 1;
+            if (hist[mid] <= t) a = mid; else b = mid;
+        }
+        dst[t] = base + a;
+    }
+}
+
 // WOR (a5/a6) and WR (a8) leaves: draw, sort, store lo + x + 1 at the offset.
 template <typename K, bool WR>
 __device__ __forceinline__ void sample_leaves(const LeafArgs &a)
@@ -292,8 +335,13 @@ __device__ __forceinline__ void sample_leaves(const LeafArgs &a)
         if (k == 0) continue;
         const LeafGeom g = leaf_geom(a, L);
         const Stream st(a.seed, WR ? P_WR : P_WOR, g.id);
-        if (!leaf_core<K, WR>(sh, st, g.r, k)) continue;
         u64 *dst = a.out + a.off[L];
+        if (WR && k > (u32)LEAF_CAP) {
+            wr_big_leaf<K>(sh, st, g.lo, g.r, k, dst);
+            __syncthreads();
+            continue;
+        }
+        if (!leaf_core<K, WR>(sh, st, g.r, k)) continue;
         const u64 base = g.lo + 1;
         for (u32 i = threadIdx.x; i < k; i += LEAF_NT) dst[i] = base + (u64)sh.stage[i];
         __syncthreads();
