@@ -228,7 +228,9 @@ double rso_log1p(double x)
 /* ------------------------------------------------------------------------- */
 
 /* stirlerr(n) = log(n!) - log(sqrt(2 pi n) (n/e)^n), integer n >= 1.
- * n <= 15: correctly rounded values (pinned vs mpmath in tests). */
+ * n <= 15: correctly rounded values (pinned vs mpmath in tests).
+ * n > 15: Stirling's series 1/(12n) - 1/(360n^3) + 1/(1260n^5)
+ * - 1/(1680n^7) + 1/(1188n^9) in powers of rn = 1/n (one division). */
 double rso_stirlerr(double n)
 {
     static const double ST[16] = {
@@ -244,15 +246,23 @@ double rso_stirlerr(double n)
     static const double S3 = 0x1.3813813813814p-11;  /* 1/1680 */
     static const double S4 = 0x1.b951e2b18ff23p-11;  /* 1/1188 */
     if (n <= 15.0) return ST[(int)n];
-    double nn = n * n;
-    if (n > 500.0) return (S0 - S1 / nn) / n;
-    if (n > 80.0)  return (S0 - (S1 - S2 / nn) / nn) / n;
-    if (n > 35.0)  return (S0 - (S1 - (S2 - S3 / nn) / nn) / nn) / n;
-    return (S0 - (S1 - (S2 - (S3 - S4 / nn) / nn) / nn) / nn) / n;
+    double rn = 1.0 / n;
+    double r2 = rn * rn;
+    return (S0 - (S1 - (S2 - (S3 - S4 * r2) * r2) * r2) * r2) * rn;
 }
 
+/* 1/(2j+1), j = 0..23, correctly rounded (the bd0 series coefficients). */
+static const double INV_ODD[24] = {
+    0x1p+0, 0x1.5555555555555p-2, 0x1.999999999999ap-3, 0x1.2492492492492p-3,
+    0x1.c71c71c71c71cp-4, 0x1.745d1745d1746p-4, 0x1.3b13b13b13b14p-4, 0x1.1111111111111p-4,
+    0x1.e1e1e1e1e1e1ep-5, 0x1.af286bca1af28p-5, 0x1.8618618618618p-5, 0x1.642c8590b2164p-5,
+    0x1.47ae147ae147bp-5, 0x1.2f684bda12f68p-5, 0x1.1a7b9611a7b96p-5, 0x1.0842108421084p-5,
+    0x1.f07c1f07c1f08p-6, 0x1.d41d41d41d41dp-6, 0x1.bacf914c1bad0p-6, 0x1.a41a41a41a41ap-6,
+    0x1.8f9c18f9c18fap-6, 0x1.7d05f417d05f4p-6, 0x1.6c16c16c16c17p-6, 0x1.5c9882b931057p-6 };
+
 /* bd0(x, np) = x log(x/np) + np - x, evaluated without cancellation
- * (Loader 2000): series in v = (x-np)/(x+np) when |x-np| < 0.1 (x+np). */
+ * (Loader 2000): series 2x sum_j v^(2j+1)/(2j+1) - (x-np) in
+ * v = (x-np)/(x+np) when |x-np| < 0.1 (x+np). */
 double rso_bd0(double x, double np)
 {
     if (fabs(x - np) < 0.1 * (x + np)) {
@@ -263,7 +273,7 @@ double rso_bd0(double x, double np)
         v = v * v;
         for (int j = 1; j < 1000; j++) {
             ej *= v;
-            double s1 = s + ej / ((j << 1) + 1);
+            double s1 = s + (j < 24 ? ej * INV_ODD[j] : ej / ((j << 1) + 1));
             if (s1 == s) return s1;
             s = s1;
         }
@@ -288,7 +298,7 @@ double rso_ldbinom(double x, double n, double p, double q)
     }
     lc = rso_stirlerr(n) - rso_stirlerr(x) - rso_stirlerr(n - x)
          - rso_bd0(x, n * p) - rso_bd0(n - x, n * q);
-    double lf = LN_2PI + rso_log(x) + rso_log1p(-x / n);
+    double lf = LN_2PI + rso_log(x * (n - x) / n);   /* log(2 pi x (n-x)/n) */
     return lc - 0.5 * lf;
 }
 

@@ -100,9 +100,7 @@ struct TreePlan {
     u64 leaf0, nleaves;     // shard's leaves
     u64 r_max;              // largest leaf range
     u64 local_count, global_offset;
-    // split phases
-    int nphase;
-    int ph_ds[8], ph_nlev[8];
+    int top;                // levels expanded by the single top CTA
     // workspace layout
     size_t o_ping_cnt, o_ping_off, o_pong_cnt, o_pong_off, o_leaf_cnt, o_leaf_off, bytes;
 };
@@ -136,26 +134,14 @@ rs_status plan_tree(int mode, u64 N, u64 n, u64 seed, int world, int rank, TreeP
     p.nleaves = 1ull << (p.D - s);
     p.leaf0 = (u64)rank << (p.D - s);
     p.r_max = (N >> p.D) + ((N & ((1ull << p.D) - 1)) != 0);
-    // split phases: depths s..D in steps of <= SPLIT_LEVELS
-    int ds = s;
-    do {
-        const int nl = (p.D - ds) < SPLIT_LEVELS ? (p.D - ds) : SPLIT_LEVELS;
-        p.ph_ds[p.nphase] = ds;
-        p.ph_nlev[p.nphase] = nl;
-        ++p.nphase;
-        ds += nl;
-    } while (ds < p.D);
-    // workspace: intermediate ping/pong (u64 cnt + off) and the leaf arrays
-    u64 wint = 1;
-    for (int i = 0; i + 1 < p.nphase; ++i) {
-        const u64 w = 1ull << (p.ph_ds[i] + p.ph_nlev[i] - s);
-        if (w > wint) wint = w;
-    }
+    // split: one CTA expands depths s..s+top, then one launch per level
+    p.top = (p.D - s) < SPLIT_TOP ? (p.D - s) : SPLIT_TOP;
+    const u64 wmax = 1ull << (p.D - s > 0 ? p.D - s - 1 : 0);   // widest intermediate level
     size_t o = 0;
-    p.o_ping_cnt = o; o = align256(o + wint * 8);
-    p.o_ping_off = o; o = align256(o + wint * 8);
-    p.o_pong_cnt = o; o = align256(o + wint * 8);
-    p.o_pong_off = o; o = align256(o + wint * 8);
+    p.o_ping_cnt = o; o = align256(o + wmax * 8);
+    p.o_ping_off = o; o = align256(o + wmax * 8);
+    p.o_pong_cnt = o; o = align256(o + wmax * 8);
+    p.o_pong_off = o; o = align256(o + wmax * 8);
     p.o_leaf_cnt = o; o = align256(o + p.nleaves * 4);
     p.o_leaf_off = o; o = align256(o + p.nleaves * 8);
     p.bytes = o;
@@ -176,22 +162,32 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
     u64 *pong_cnt = (u64 *)(ws + p.o_pong_cnt), *pong_off = (u64 *)(ws + p.o_pong_off);
     u32 *leaf_cnt = (u32 *)(ws + p.o_leaf_cnt);
     u64 *leaf_off = (u64 *)(ws + p.o_leaf_off);
-    const u64 *in_cnt = nullptr, *in_off = nullptr;
     Span sp_split(0, st);
-    for (int i = 0; i < p.nphase; ++i) {
+    {   // top levels s .. s+top in one CTA
         SplitArgs a;
         memset(&a, 0, sizeof a);
         a.N = p.N; a.seed = p.seed; a.wr = (p.mode == RS_MODE_WR);
-        a.ds = p.ph_ds[i]; a.nlev = p.ph_nlev[i];
-        a.node0 = (u64)p.rank << (a.ds - p.s);
+        a.ds = p.s; a.nlev = p.top; a.node0 = (u64)p.rank;
+        a.root_cnt = p.root_cnt; a.root_off = 0;        // offsets local to the shard
+        if (p.s + p.top == p.D) { a.leaf_cnt = leaf_cnt; a.leaf_off = leaf_off; }
+        else { a.out_cnt = ping_cnt; a.out_off = ping_off; }
+        k_split<<<1, SPLIT_NT, 0, st>>>(a);
+        ++t_launches;
+    }
+    const u64 *in_cnt = ping_cnt, *in_off = ping_off;
+    for (int d = p.s + p.top; d < p.D; ++d) {         // one launch per deeper level
+        LevelArgs a;
+        memset(&a, 0, sizeof a);
+        a.N = p.N; a.seed = p.seed; a.wr = (p.mode == RS_MODE_WR); a.d = d;
+        a.width = 1ull << (d - p.s);
+        a.node0 = (u64)p.rank << (d - p.s);
         a.in_cnt = in_cnt; a.in_off = in_off;
-        a.root_cnt = p.root_cnt; a.root_off = 0;       // offsets local to the shard
-        const bool last = (i + 1 == p.nphase);
-        u64 *oc = (i & 1) ? pong_cnt : ping_cnt, *oo = (i & 1) ? pong_off : ping_off;
-        if (last) { a.leaf_cnt = leaf_cnt; a.leaf_off = leaf_off; }
+        const bool flip = ((d - p.s - p.top) & 1) == 0;
+        u64 *oc = flip ? pong_cnt : ping_cnt, *oo = flip ? pong_off : ping_off;
+        if (d + 1 == p.D) { a.leaf_cnt = leaf_cnt; a.leaf_off = leaf_off; }
         else { a.out_cnt = oc; a.out_off = oo; }
-        const u64 grid = 1ull << (a.ds - p.s);
-        k_split<<<(unsigned)grid, SPLIT_NT, 0, st>>>(a);
+        const u64 grid = (a.width + LEVEL_NT - 1) / LEVEL_NT;
+        k_split_level<<<(unsigned)grid, LEVEL_NT, 0, st>>>(a);
         ++t_launches;
         in_cnt = oc; in_off = oo;
     }
@@ -202,7 +198,7 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
     la.N = p.N; la.seed = p.seed; la.D = p.D;
     la.leaf0 = p.leaf0; la.nleaves = p.nleaves;
     la.cnt = leaf_cnt; la.off = leaf_off; la.out = out;
-    const bool wide = p.r_max > 0x100000000ull;
+    const bool wide = p.r_max >= 0xffffffffull;   // u32 keys need x < 0xffffffff (EMPTY)
     const u64 max_grid = 0x7fffffffull;
     if (p.comp) {
         la.out_base = p.shard_lo;
@@ -222,12 +218,12 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         const unsigned grid = (unsigned)(p.nleaves < max_grid ? p.nleaves : max_grid);
         const bool wr = (p.mode == RS_MODE_WR);
         if (wide) {
-            const size_t sm = sizeof(LeafShared<u64>);
+            const size_t sm = sizeof(TableShared<u64>) > sizeof(LeafShared<u64>) ? sizeof(TableShared<u64>) : sizeof(LeafShared<u64>);
             auto kern = wr ? k_leaf_wr64 : k_leaf_wor64;
             set_smem(kern, sm);
             kern<<<grid, LEAF_NT, sm, st>>>(la);
         } else {
-            const size_t sm = sizeof(LeafShared<u32>);
+            const size_t sm = sizeof(TableShared<u32>) > sizeof(LeafShared<u32>) ? sizeof(TableShared<u32>) : sizeof(LeafShared<u32>);
             auto kern = wr ? k_leaf_wr32 : k_leaf_wor32;
             set_smem(kern, sm);
             kern<<<grid, LEAF_NT, sm, st>>>(la);

@@ -56,6 +56,26 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split(SplitArgs a)
     }
 }
 
+__global__ void __launch_bounds__(LEVEL_NT, 8) k_split_level(LevelArgs a)
+{
+    const u64 j = (u64)blockIdx.x * LEVEL_NT + threadIdx.x;
+    if (j >= a.width) return;
+    const u64 k = a.in_cnt[j], off = a.in_off[j];
+    const u64 x = split_node(a.wr != 0, a.N, a.d, a.node0 + j, k, a.seed);
+    if (a.leaf_cnt) {
+        if (k > 0xffffffffull) atomicOr(&g_rs_errors, 1u);
+        a.leaf_cnt[2 * j] = (u32)x;
+        a.leaf_cnt[2 * j + 1] = (u32)(k - x);
+        a.leaf_off[2 * j] = off;
+        a.leaf_off[2 * j + 1] = off + x;
+    } else {
+        a.out_cnt[2 * j] = x;
+        a.out_cnt[2 * j + 1] = k - x;
+        a.out_off[2 * j] = off;
+        a.out_off[2 * j + 1] = off + x;
+    }
+}
+
 // ===========================================================================
 // Leaf machinery: sorted first-k-distinct (Algorithm H, sorted
 // per P:356-374) or sorted multiset (WR), entirely in shared memory.
@@ -84,7 +104,8 @@ template <> struct Drawer<u32> {
     Stream st; u64 r; u32 thresh;
     __device__ Drawer(const Stream &s, u64 r_) : st(s), r(r_)
     {
-        thresh = (u32)(0x100000000ull % r_);
+        // 2^32 mod r (0 for powers of two: Lemire never rejects)
+        thresh = (r_ & (r_ - 1)) ? (u32)(0u - (u32)r_) % (u32)r_ : 0u;
     }
     __device__ __forceinline__ u32 fix(u32 w, u64 j) const
     {
@@ -110,7 +131,10 @@ template <> struct Drawer<u32> {
 template <> struct Drawer<u64> {
     static constexpr int EPB = 2;
     Stream st; u64 r; u64 thresh;
-    __device__ Drawer(const Stream &s, u64 r_) : st(s), r(r_) { thresh = (0 - r_) % r_; }
+    __device__ Drawer(const Stream &s, u64 r_) : st(s), r(r_)
+    {
+        thresh = (r_ & (r_ - 1)) ? (0 - r_) % r_ : 0;   // 2^64 mod r
+    }
     __device__ __forceinline__ u64 fix(u64 w, u64 j) const
     {
         u64 lo = w * r, hi = __umul64hi(w, r);
@@ -348,10 +372,145 @@ __device__ __forceinline__ void sample_leaves(const LeafArgs &a)
     }
 }
 
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_wor32(LeafArgs a) { sample_leaves<u32, false>(a); }
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_wor64(LeafArgs a) { sample_leaves<u64, false>(a); }
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_wr32(LeafArgs a) { sample_leaves<u32, true>(a); }
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_wr64(LeafArgs a) { sample_leaves<u64, true>(a); }
+// ===========================================================================
+// v2 leaf: Algorithm H with the paper's SORTED hash table (P:360-368,
+// P:582-594).  The table has M ~ 2k slots plus an overflow area on the right
+// ("n additional table entries ... unnecessary to wrap around");
+// the hash is the monotone home(x) = floor(x M / 2^cr) ("extracting the most
+// significant bits").  Insertion keeps every cluster sorted by
+// "skipping elements smaller than k and shifting the cluster elements larger
+// than k one position to the right": a thread carrying x walks
+// right from home(x) past smaller keys and CAS-swaps x into the first slot
+// holding a larger key (or EMPTY), then carries the displaced key onward.
+// Slot contents only decrease and keys only move right, so concurrent
+// insertion terminates and yields the unique ordered-probing table of the key
+// set.  Equal keys: WOR drops the second copy (Algorithm H's rejection);
+// WR keeps both.  Scanning the table in order then IS the sorted sample.
+// ===========================================================================
+constexpr int T_OVF = 256;                          // overflow slots (no wrap-around)
+constexpr int T_MAX = 2 * LEAF_CAP + T_OVF;         // slots for k <= LEAF_CAP
+
+template <typename K> struct Empty;
+template <> struct Empty<u32> { static constexpr u32 v = 0xffffffffu; };
+template <> struct Empty<u64> { static constexpr u64 v = ~0ull; };
+
+template <typename K>
+struct TableShared {
+    K T[T_MAX];
+    u32 wcnt[LEAF_NT / 32];
+    u32 wpre[LEAF_NT / 32 + 1];
+};
+
+__device__ __forceinline__ u32 cas_(u32 *p, u32 c, u32 v) { return atomicCAS(p, c, v); }
+__device__ __forceinline__ u64 cas_(u64 *p, u64 c, u64 v)
+{
+    return (u64)atomicCAS((unsigned long long *)p, (unsigned long long)c, (unsigned long long)v);
+}
+
+// Insert x; returns 1 if x was a duplicate (WOR: dropped), 2 on overflow.
+template <typename K, bool WR>
+__device__ __forceinline__ int table_insert(K *T, K x, u32 p, u32 limit)
+{
+    for (;;) {
+        const K y = *(volatile K *)&T[p];
+        if (!WR && y == x) return 1;
+        if (y < x || (WR && y == x)) {           // skip smaller (and equal, WR) keys
+            if (++p >= limit) return 2;
+            continue;
+        }
+        const K old = cas_(&T[p], y, x);       // y > x or EMPTY: take the slot
+        if (old != y) continue;                // slot changed under us: re-read
+        if (y == Empty<K>::v) return 0;
+        x = y;                                 // carry the displaced key right
+        if (++p >= limit) return 2;
+    }
+}
+
+template <typename K, bool WR>
+__device__ __forceinline__ void sample_leaves_v2(const LeafArgs &a)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TableShared<K> &sh = *reinterpret_cast<TableShared<K> *>(smem_raw);
+    constexpr int EPB = Drawer<K>::EPB;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (u64 L = blockIdx.x; L < a.nleaves; L += gridDim.x) {
+        const u32 k = a.cnt[L];
+        if (k == 0) continue;
+        const LeafGeom g = leaf_geom(a, L);
+        const Stream st(a.seed, WR ? P_WR : P_WOR, g.id);
+        u64 *dst = a.out + a.off[L];
+        if (k > (u32)LEAF_CAP) {                 // beyond on-chip capacity
+            if (WR) wr_big_leaf<K>(*reinterpret_cast<LeafShared<K> *>(smem_raw), st, g.lo, g.r, k, dst);
+            else if (tid == 0) atomicOr(&g_rs_errors, 1u);
+            __syncthreads();
+            continue;
+        }
+        const u32 M = ((2 * k + 255) / 256) * 256;    // ~2k slots, multiple of 256
+        const u32 TS = M + T_OVF;                     // scanned slots (multiple of 256)
+        const int cr = ceil_log2(g.r);
+        for (u32 i = tid; i < TS; i += LEAF_NT) sh.T[i] = Empty<K>::v;
+        __syncthreads();
+        const Drawer<K> dr(st, g.r);
+        u32 J0 = 0, J = k, have = 0;
+        bool overflow = false;
+        for (;;) {                                     // rounds of Algorithm H
+            int dups = 0;
+            const u32 q0 = J0 / EPB, q1 = (J + EPB - 1) / EPB;
+            for (u32 q = q0 + tid; q < q1; q += LEAF_NT) {
+                K v[EPB];
+                dr.block(q, v);
+#pragma unroll
+                for (int w = 0; w < EPB; ++w) {
+                    const u32 j = q * EPB + w;
+                    if (j < J0 || j >= J) continue;
+                    const u32 home = (u32)(((unsigned __int128)v[w] * M) >> cr);
+                    const int rc = table_insert<K, WR>(sh.T, v[w], home, TS);
+                    dups += (rc == 1);
+                    overflow |= (rc == 2);
+                }
+            }
+            const int nd = __syncthreads_count(dups);
+            if (__syncthreads_or(overflow)) break;
+            have += (J - J0) - nd;
+            if (WR || have == k) break;
+            J0 = J;
+            J += k - have;                             // next round: k - |S| draws
+        }
+        if (__syncthreads_or(overflow)) {
+            if (tid == 0) atomicOr(&g_rs_errors, 1u);
+            continue;
+        }
+        // in-place per-warp compaction of the table (warp w owns TS/8 slots)
+        const u32 per = TS / (LEAF_NT / 32);
+        K *reg = sh.T + wid * per;
+        u32 c = 0;
+        for (u32 i = 0; i < per; i += 32) {
+            const K v = reg[i + lane];
+            const bool occ = v != Empty<K>::v;
+            const u32 m = __ballot_sync(0xffffffffu, occ);
+            if (occ) reg[c + __popc(m & ((1u << lane) - 1))] = v;
+            c += __popc(m);
+            __syncwarp();
+        }
+        if (lane == 0) sh.wcnt[wid] = c;
+        __syncthreads();
+        if (tid == 0) {
+            u32 acc = 0;
+            for (int w = 0; w < LEAF_NT / 32; ++w) { sh.wpre[w] = acc; acc += sh.wcnt[w]; }
+            sh.wpre[LEAF_NT / 32] = acc;
+        }
+        __syncthreads();
+        const u32 o = sh.wpre[wid];
+        const u64 base = g.lo + 1;
+        for (u32 t = lane; t < c; t += 32) dst[o + t] = base + (u64)reg[t];
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(LEAF_NT) k_leaf_wor32(LeafArgs a) { sample_leaves_v2<u32, false>(a); }
+__global__ void __launch_bounds__(LEAF_NT) k_leaf_wor64(LeafArgs a) { sample_leaves_v2<u64, false>(a); }
+__global__ void __launch_bounds__(LEAF_NT) k_leaf_wr32(LeafArgs a) { sample_leaves_v2<u32, true>(a); }
+__global__ void __launch_bounds__(LEAF_NT) k_leaf_wr64(LeafArgs a) { sample_leaves_v2<u64, true>(a); }
 
 // Complement leaves (a7): emit [lo, lo+r) minus the core leaf's
 // e excluded values.  Output index t of the leaf maps to offset t + j(t),

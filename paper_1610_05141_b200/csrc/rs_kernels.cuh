@@ -86,6 +86,20 @@ struct SplitArgs {
 
 __global__ void __launch_bounds__(SPLIT_NT) k_split(SplitArgs a);
 
+// One tree level across the whole GPU: thread j splits node (d, node0 + j).
+constexpr int LEVEL_NT = 128;
+constexpr int SPLIT_TOP = 10;                    // levels expanded by the single top CTA
+struct LevelArgs {
+    u64 N, seed;
+    int wr, d;
+    u64 node0, width;
+    const u64 *in_cnt, *in_off;
+    u64 *out_cnt, *out_off;        // next level (intermediate) or
+    u32 *leaf_cnt;                 // leaf level: u32 counts + u64 offsets
+    u64 *leaf_off;
+};
+__global__ void __launch_bounds__(LEVEL_NT, 8) k_split_level(LevelArgs a);
+
 // ---------------------------------------------------------------------------
 // Leaf kernels (rows a5/a6/a7/a8).
 // ---------------------------------------------------------------------------
