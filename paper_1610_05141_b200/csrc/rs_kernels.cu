@@ -399,6 +399,7 @@ struct TableShared {
     K T[T_MAX];
     u32 wcnt[LEAF_NT / 32];
     u32 wpre[LEAF_NT / 32 + 1];
+    u32 ndup;
 };
 
 __device__ __forceinline__ u32 cas_(u32 *p, u32 c, u32 v) { return atomicCAS(p, c, v); }
@@ -449,6 +450,7 @@ __device__ __forceinline__ void sample_leaves_v2(const LeafArgs &a)
         const u32 TS = M + T_OVF;                     // scanned slots (multiple of 256)
         const int cr = ceil_log2(g.r);
         for (u32 i = tid; i < TS; i += LEAF_NT) sh.T[i] = Empty<K>::v;
+        if (tid == 0) sh.ndup = 0;
         __syncthreads();
         const Drawer<K> dr(st, g.r);
         u32 J0 = 0, J = k, have = 0;
@@ -469,10 +471,15 @@ __device__ __forceinline__ void sample_leaves_v2(const LeafArgs &a)
                     overflow |= (rc == 2);
                 }
             }
-            const int nd = __syncthreads_count(dups);
+            const u32 wd = __reduce_add_sync(0xffffffffu, (u32)dups);   // duplicates this round
+            if (lane == 0 && wd) atomicAdd(&sh.ndup, wd);
             if (__syncthreads_or(overflow)) break;
+            const u32 nd = sh.ndup;
             have += (J - J0) - nd;
             if (WR || have == k) break;
+            __syncthreads();                           // all threads have read ndup
+            if (tid == 0) sh.ndup = 0;
+            __syncthreads();
             J0 = J;
             J += k - have;                             // next round: k - |S| draws
         }
