@@ -427,12 +427,60 @@ __device__ __forceinline__ int table_insert(K *T, K x, u32 p, u32 limit)
     }
 }
 
+template <typename K>
+__device__ __forceinline__ u32 home_of(K x, u32 M, int cr);
+template <>
+__device__ __forceinline__ u32 home_of<u32>(u32 x, u32 M, int cr) { return (u32)(((u64)x * M) >> cr); }
+template <>
+__device__ __forceinline__ u32 home_of<u64>(u64 x, u32 M, int cr)
+{
+    return (u32)(((unsigned __int128)x * M) >> cr);
+}
+
+// Insert a lane's pending draws q[0..n) with ONE loop, so a lane that
+// finishes a short walk starts its next value in the same iteration (the
+// warp then runs ~the sum of its lanes' walks, not 4 x the slowest walk).
+// q is a register shift-queue (compile-time indices only).  Returns the
+// number of duplicates (WOR) and sets *ovf on overflow.
+template <typename K, bool WR, int NV>
+__device__ __forceinline__ u32 insert_all(K *T, K (&q)[NV], int n, u32 M, int cr, u32 limit, bool *ovf)
+{
+    u32 dups = 0;
+    K x = q[0];
+    u32 p = home_of<K>(x, M, cr);
+    while (n > 0) {
+        bool done = false;
+        const K y = *(volatile K *)&T[p];
+        if (!WR && y == x) {                       // Algorithm H: reject the duplicate
+            ++dups;
+            done = true;
+        } else if (y < x || (WR && y == x)) {      // skip smaller keys
+            if (++p >= limit) { *ovf = true; return dups; }
+        } else {
+            const K old = cas_(&T[p], y, x);       // y > x or EMPTY: take the slot
+            if (old == y) {
+                if (y == Empty<K>::v) done = true;
+                else { x = y; if (++p >= limit) { *ovf = true; return dups; } }   // carry y right
+            }
+        }
+        if (done) {
+#pragma unroll
+            for (int t = 0; t + 1 < NV; ++t) q[t] = q[t + 1];
+            --n;
+            x = q[0];
+            p = home_of<K>(x, M, cr);
+        }
+    }
+    return dups;
+}
+
 template <typename K, bool WR>
 __device__ __forceinline__ void sample_leaves_v2(const LeafArgs &a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TableShared<K> &sh = *reinterpret_cast<TableShared<K> *>(smem_raw);
     constexpr int EPB = Drawer<K>::EPB;
+    constexpr int BPT = LEAF_EPT / EPB;               // Philox blocks per thread per round
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     for (u64 L = blockIdx.x; L < a.nleaves; L += gridDim.x) {
         const u32 k = a.cnt[L];
@@ -449,29 +497,39 @@ __device__ __forceinline__ void sample_leaves_v2(const LeafArgs &a)
         const u32 M = ((2 * k + 255) / 256) * 256;    // ~2k slots, multiple of 256
         const u32 TS = M + T_OVF;                     // scanned slots (multiple of 256)
         const int cr = ceil_log2(g.r);
-        for (u32 i = tid; i < TS; i += LEAF_NT) sh.T[i] = Empty<K>::v;
+        {
+            uint4 *T4 = reinterpret_cast<uint4 *>(sh.T);
+            const uint4 e4 = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+            for (u32 i = tid; i < TS * sizeof(K) / 16; i += LEAF_NT) T4[i] = e4;
+        }
         if (tid == 0) sh.ndup = 0;
         __syncthreads();
         const Drawer<K> dr(st, g.r);
         u32 J0 = 0, J = k, have = 0;
         bool overflow = false;
         for (;;) {                                     // rounds of Algorithm H
-            int dups = 0;
             const u32 q0 = J0 / EPB, q1 = (J + EPB - 1) / EPB;
-            for (u32 q = q0 + tid; q < q1; q += LEAF_NT) {
-                K v[EPB];
-                dr.block(q, v);
+            // this thread's draws of the round, packed into a register queue
+            K v[LEAF_EPT];
+            int nv = 0;
+#pragma unroll
+            for (int s = 0; s < BPT; ++s) {
+                const u32 q = q0 + tid + LEAF_NT * s;
+                K b[EPB];
+                if (q < q1) dr.block(q, b);
 #pragma unroll
                 for (int w = 0; w < EPB; ++w) {
                     const u32 j = q * EPB + w;
-                    if (j < J0 || j >= J) continue;
-                    const u32 home = (u32)(((unsigned __int128)v[w] * M) >> cr);
-                    const int rc = table_insert<K, WR>(sh.T, v[w], home, TS);
-                    dups += (rc == 1);
-                    overflow |= (rc == 2);
+                    const bool ok = q < q1 && j >= J0 && j < J;
+                    // append b[w] at position nv (unrolled select: no local memory)
+#pragma unroll
+                    for (int t = 0; t < LEAF_EPT; ++t)
+                        if (ok && t == nv) v[t] = b[w];
+                    nv += ok;
                 }
             }
-            const u32 wd = __reduce_add_sync(0xffffffffu, (u32)dups);   // duplicates this round
+            const u32 dups = nv ? insert_all<K, WR, LEAF_EPT>(sh.T, v, nv, M, cr, TS, &overflow) : 0u;
+            const u32 wd = __reduce_add_sync(0xffffffffu, dups);     // duplicates this round
             if (lane == 0 && wd) atomicAdd(&sh.ndup, wd);
             if (__syncthreads_or(overflow)) break;
             const u32 nd = sh.ndup;
@@ -514,9 +572,9 @@ __device__ __forceinline__ void sample_leaves_v2(const LeafArgs &a)
     }
 }
 
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_wor32(LeafArgs a) { sample_leaves_v2<u32, false>(a); }
+__global__ void __launch_bounds__(LEAF_NT, 4) k_leaf_wor32(LeafArgs a) { sample_leaves_v2<u32, false>(a); }
 __global__ void __launch_bounds__(LEAF_NT) k_leaf_wor64(LeafArgs a) { sample_leaves_v2<u64, false>(a); }
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_wr32(LeafArgs a) { sample_leaves_v2<u32, true>(a); }
+__global__ void __launch_bounds__(LEAF_NT, 4) k_leaf_wr32(LeafArgs a) { sample_leaves_v2<u32, true>(a); }
 __global__ void __launch_bounds__(LEAF_NT) k_leaf_wr64(LeafArgs a) { sample_leaves_v2<u64, true>(a); }
 
 // Complement leaves (a7): emit [lo, lo+r) minus the core leaf's

@@ -115,9 +115,9 @@ struct LeafArgs {
     u64 *out;
 };
 
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_wor32(LeafArgs a);
+__global__ void __launch_bounds__(LEAF_NT, 4) k_leaf_wor32(LeafArgs a);
 __global__ void __launch_bounds__(LEAF_NT) k_leaf_wor64(LeafArgs a);
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_wr32(LeafArgs a);
+__global__ void __launch_bounds__(LEAF_NT, 4) k_leaf_wr32(LeafArgs a);
 __global__ void __launch_bounds__(LEAF_NT) k_leaf_wr64(LeafArgs a);
 __global__ void __launch_bounds__(LEAF_NT) k_leaf_comp32(LeafArgs a);
 __global__ void __launch_bounds__(LEAF_NT) k_leaf_comp64(LeafArgs a);
