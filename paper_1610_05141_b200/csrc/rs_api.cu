@@ -102,7 +102,7 @@ struct TreePlan {
     u64 local_count, global_offset;
     int top;                // levels expanded by the single top CTA
     // workspace layout
-    size_t o_ping_cnt, o_ping_off, o_pong_cnt, o_pong_off, o_leaf_cnt, o_leaf_off, bytes;
+    size_t o_ping_cnt, o_ping_off, o_pong_cnt, o_pong_off, o_leaf_cnt, o_leaf_off, o_spill, bytes;
 };
 
 rs_status plan_tree(int mode, u64 N, u64 n, u64 seed, int world, int rank, TreePlan &p)
@@ -144,6 +144,7 @@ rs_status plan_tree(int mode, u64 N, u64 n, u64 seed, int world, int rank, TreeP
     p.o_pong_off = o; o = align256(o + wmax * 8);
     p.o_leaf_cnt = o; o = align256(o + p.nleaves * 4);
     p.o_leaf_off = o; o = align256(o + p.nleaves * 8);
+    p.o_spill = o; o = align256(o + (p.nleaves + 1) * 4);   // spill count + list
     p.bytes = o;
     return RS_OK;
 }
@@ -152,6 +153,26 @@ template <typename F>
 void set_smem(F *kernel, size_t bytes)
 {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+// Persistent leaf grid: every resident CTA slot once (occupancy x SMs),
+// capped by the number of work items; the kernels grid-stride over leaves.
+unsigned leaf_grid(const void *kern, int threads, size_t smem, u64 work)
+{
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, smem) != cudaSuccess || per < 1)
+        per = 1;
+    const u64 g = (u64)sms * (u64)per;
+    return (unsigned)(work < g ? (work ? work : 1) : g);
 }
 
 // Launch the split phases and the leaf kernel of a tree plan.
@@ -198,37 +219,44 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
     la.N = p.N; la.seed = p.seed; la.D = p.D;
     la.leaf0 = p.leaf0; la.nleaves = p.nleaves;
     la.cnt = leaf_cnt; la.off = leaf_off; la.out = out;
-    const bool wide = p.r_max >= 0xffffffffull;   // u32 keys need x < 0xffffffff (EMPTY)
-    const u64 max_grid = 0x7fffffffull;
+    const bool wide = p.r_max >= 0xffffffffull;   // u32 keys hold offsets < 2^32
+    const bool wr = (p.mode == RS_MODE_WR);
+    void (*kern)(LeafArgs);
+    size_t sm;
     if (p.comp) {
         la.out_base = p.shard_lo;
         la.tiles_per_leaf = (p.r_max + COMP_TILE - 1) / COMP_TILE;
-        u64 total = p.nleaves * la.tiles_per_leaf;
-        const unsigned grid = (unsigned)(total < max_grid ? total : max_grid);
-        if (wide) {
-            const size_t sm = sizeof(LeafShared<u64>);
-            set_smem(k_leaf_comp64, sm);
-            k_leaf_comp64<<<grid, LEAF_NT, sm, st>>>(la);
-        } else {
-            const size_t sm = sizeof(LeafShared<u32>);
-            set_smem(k_leaf_comp32, sm);
-            k_leaf_comp32<<<grid, LEAF_NT, sm, st>>>(la);
-        }
+        kern = wide ? k_leaf_comp64 : k_leaf_comp32;
+    } else if (!wide) {
+        // common path: warp per leaf; leaves it cannot hold go to a spill
+        // list that the CTA kernel completes right after (usually empty)
+        u32 *spill_n = (u32 *)(ws + p.o_spill);
+        la.spill_n = spill_n;
+        la.spill = spill_n + 1;
+        cudaMemsetAsync(spill_n, 0, 4, st);
+        void (*wk)(LeafArgs) = wr ? k_leaf_warp_wr : k_leaf_warp_wor;
+        const size_t wsm = sizeof(WarpLeaf) * WL_WARPS;
+        const u64 wgrid = (p.nleaves + WL_WARPS - 1) / WL_WARPS;
+        const unsigned g1 = leaf_grid((const void *)wk, 32 * WL_WARPS, wsm, wgrid);
+        wk<<<g1, 32 * WL_WARPS, wsm, st>>>(la);
+        ++t_launches;
+        LeafArgs lb = la;
+        lb.spill = nullptr; lb.spill_n = nullptr;
+        lb.list = spill_n + 1; lb.list_n = spill_n;
+        kern = wr ? k_leaf_wr32 : k_leaf_wor32;
+        sm = sizeof(SLeaf<u32>);
+        const unsigned g2 = leaf_grid((const void *)kern, LEAF_NT, sm, 2ull * 148);
+        kern<<<g2, LEAF_NT, sm, st>>>(lb);
+        ++t_launches;
+        sp_leaf.end();
+        return cuda_ok();
     } else {
-        const unsigned grid = (unsigned)(p.nleaves < max_grid ? p.nleaves : max_grid);
-        const bool wr = (p.mode == RS_MODE_WR);
-        if (wide) {
-            const size_t sm = sizeof(TableShared<u64>) > sizeof(LeafShared<u64>) ? sizeof(TableShared<u64>) : sizeof(LeafShared<u64>);
-            auto kern = wr ? k_leaf_wr64 : k_leaf_wor64;
-            set_smem(kern, sm);
-            kern<<<grid, LEAF_NT, sm, st>>>(la);
-        } else {
-            const size_t sm = sizeof(TableShared<u32>) > sizeof(LeafShared<u32>) ? sizeof(TableShared<u32>) : sizeof(LeafShared<u32>);
-            auto kern = wr ? k_leaf_wr32 : k_leaf_wor32;
-            set_smem(kern, sm);
-            kern<<<grid, LEAF_NT, sm, st>>>(la);
-        }
+        kern = wr ? k_leaf_wr64 : k_leaf_wor64;
     }
+    sm = wide ? sizeof(SLeaf<u64>) : sizeof(SLeaf<u32>);
+    const u64 work = p.comp ? p.nleaves * la.tiles_per_leaf : p.nleaves;
+    const unsigned grid = leaf_grid((const void *)kern, LEAF_NT, sm, work);
+    kern<<<grid, LEAF_NT, sm, st>>>(la);
     ++t_launches;
     sp_leaf.end();
     return cuda_ok();

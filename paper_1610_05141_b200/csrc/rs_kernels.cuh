@@ -14,7 +14,7 @@ constexpr int SPLIT_NT = 256;
 constexpr int SPLIT_LEVELS = 11;                 // levels expanded per split phase
 constexpr int SPLIT_WIDTH = 1 << SPLIT_LEVELS;   // nodes per CTA at the phase's last level
 
-constexpr int LEAF_NT = 256;                     // threads per leaf CTA
+constexpr int LEAF_NT = 512;                     // threads per leaf CTA
 constexpr int LEAF_CAP = 2048;                   // draws held on chip per leaf
 constexpr int LEAF_EPT = LEAF_CAP / LEAF_NT;     // elements per thread
 
@@ -113,14 +113,23 @@ struct LeafArgs {
     u64 out_base;          // complement: subtracted from leaf output positions
     u64 tiles_per_leaf;    // complement tiling
     u64 *out;
+    u32 *spill;            // warp kernel: leaves it could not hold on chip (appended)
+    u32 *spill_n;          //   ... and their count; the CTA kernel then walks this list
+    const u32 *list;       // CTA kernel: if set, process only list[0 .. *list_n)
+    const u32 *list_n;
 };
 
-__global__ void __launch_bounds__(LEAF_NT, 4) k_leaf_wor32(LeafArgs a);
+__global__ void __launch_bounds__(LEAF_NT) k_leaf_wor32(LeafArgs a);
 __global__ void __launch_bounds__(LEAF_NT) k_leaf_wor64(LeafArgs a);
-__global__ void __launch_bounds__(LEAF_NT, 4) k_leaf_wr32(LeafArgs a);
+__global__ void __launch_bounds__(LEAF_NT) k_leaf_wr32(LeafArgs a);
 __global__ void __launch_bounds__(LEAF_NT) k_leaf_wr64(LeafArgs a);
 __global__ void __launch_bounds__(LEAF_NT) k_leaf_comp32(LeafArgs a);
 __global__ void __launch_bounds__(LEAF_NT) k_leaf_comp64(LeafArgs a);
+
+// Warp-per-leaf kernels (u32 keys): the common path; see rs_leaf.cuh.
+constexpr int WL_WARPS = 4;                      // warps (independent leaves) per CTA
+__global__ void __launch_bounds__(32 * WL_WARPS, 4) k_leaf_warp_wor(LeafArgs a);
+__global__ void __launch_bounds__(32 * WL_WARPS, 4) k_leaf_warp_wr(LeafArgs a);
 
 // ---------------------------------------------------------------------------
 // Bernoulli (row a9): one chunk per CTA (dynamic ticket order), geometric

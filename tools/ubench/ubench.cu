@@ -1,0 +1,99 @@
+// Microbenchmarks of the primitives the leaf kernel is built from (sm_100a):
+// Philox4x32-10 blocks, shared-memory atomics / loads / stores at random
+// addresses, and the global write ceiling.  Dev tool: numbers go to DESIGN.md.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+typedef uint32_t u32; typedef uint64_t u64;
+
+__device__ __forceinline__ uint4 philox(u32 c0, u32 c1, u32 c2, u32 c3, u32 k0, u32 k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    u32 h0 = __umulhi(0xD2511F53u, c0), l0 = 0xD2511F53u * c0;
+    u32 h1 = __umulhi(0xCD9E8D57u, c2), l1 = 0xCD9E8D57u * c2;
+    c0 = h1 ^ c1 ^ k0; c1 = l1; c2 = h0 ^ c3 ^ k1; c3 = l0;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+  return make_uint4(c0, c1, c2, c3);
+}
+
+__global__ void k_philox(u32 iters, u32 *out, u32 seed) {
+  u32 acc = 0;
+  u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+  for (u32 i = 0; i < iters; ++i) {
+    uint4 w = philox(i, 2u << 24, t, 0, seed, 7);
+    acc ^= w.x ^ w.y ^ w.z ^ w.w;
+  }
+  if (acc == 0x12345678) out[0] = acc;
+}
+
+// random smem ops: each thread does iters ops at pseudo-random addresses in a 16 KB table
+template <int OP>
+__global__ void k_smem(u32 iters, u32 *out) {
+  __shared__ u32 T[4096];
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) T[i] = i;
+  __syncthreads();
+  u32 x = threadIdx.x * 0x9E3779B9u + blockIdx.x, acc = 0;
+  for (u32 i = 0; i < iters; ++i) {
+    x = x * 1664525u + 1013904223u;
+    u32 a = x >> 20;  // 0..4095
+    if (OP == 0) acc += atomicAdd(&T[a], 1u);
+    else if (OP == 1) acc += atomicOr(&T[a], 1u << (x & 31));
+    else if (OP == 2) acc += T[a];
+    else if (OP == 3) T[a] = x;
+    else if (OP == 4) atomicAdd(&T[a], 1u);   // no return (RED)
+    else if (OP == 5) acc += atomicCAS(&T[a], acc, x);
+  }
+  __syncthreads();
+  if (acc == 0x12345678 || T[threadIdx.x] == 0x12345679) out[0] = acc;
+}
+
+// baseline: the LCG loop alone
+__global__ void k_lcg(u32 iters, u32 *out) {
+  u32 x = threadIdx.x * 0x9E3779B9u + blockIdx.x, acc = 0;
+  for (u32 i = 0; i < iters; ++i) { x = x * 1664525u + 1013904223u; acc += x >> 20; }
+  if (acc == 0x12345678) out[0] = acc;
+}
+
+template <int V>
+__global__ void k_fill(u64 *out, u64 n) {
+  u64 i0 = (u64)blockIdx.x * blockDim.x + threadIdx.x, st = (u64)gridDim.x * blockDim.x;
+  if (V == 1) { for (u64 i = i0; i < n; i += st) out[i] = i + 1; }
+  if (V == 2) { for (u64 i = i0; i < n / 2; i += st) { ulonglong2 v = make_ulonglong2(2*i+1, 2*i+2); reinterpret_cast<ulonglong2*>(out)[i] = v; } }
+  if (V == 4) { for (u64 i = i0; i < n / 4; i += st) {
+      u64 a = 4*i+1, b = a+1, c = a+2, d = a+3; u64 *p = out + 4*i;
+      asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" :: "l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory"); } }
+}
+
+#define TIME(label, launch, work, unit) do { \
+  launch; cudaDeviceSynchronize(); cudaEventRecord(e0); for (int r = 0; r < 3; ++r) { launch; } cudaEventRecord(e1); \
+  cudaEventSynchronize(e1); float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 3; \
+  printf("%-28s %9.3f ms  %10.3f %s\n", label, ms, (double)(work) / (ms * 1e-3) / 1e9, unit); } while (0)
+
+int main() {
+  cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
+  int sms = p.multiProcessorCount;
+  printf("%s SMs=%d\n", p.name, sms);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  u32 *o; cudaMalloc(&o, 64);
+  int grid = sms * 8, nt = 256; u32 it = 4096;
+  double threads = (double)grid * nt;
+  TIME("philox blocks", (k_philox<<<grid, nt>>>(it, o, 1)), threads * it, "G blocks/s");
+  TIME("lcg loop", (k_lcg<<<grid, nt>>>(it * 4, o)), threads * it * 4, "G it/s");
+  TIME("smem atomicAdd ret", (k_smem<0><<<grid, nt>>>(it, o)), threads * it, "G ops/s");
+  TIME("smem atomicOr ret", (k_smem<1><<<grid, nt>>>(it, o)), threads * it, "G ops/s");
+  TIME("smem LDS random", (k_smem<2><<<grid, nt>>>(it, o)), threads * it, "G ops/s");
+  TIME("smem STS random", (k_smem<3><<<grid, nt>>>(it, o)), threads * it, "G ops/s");
+  TIME("smem atomicAdd noret", (k_smem<4><<<grid, nt>>>(it, o)), threads * it, "G ops/s");
+  TIME("smem atomicCAS", (k_smem<5><<<grid, nt>>>(it, o)), threads * it, "G ops/s");
+  u64 n = 1ull << 32; u64 *buf; cudaMalloc(&buf, n * 8);
+  for (int g : {sms * 4, sms * 8, sms * 16}) {
+    char l[64];
+    snprintf(l, 64, "fill u64 v1 grid=%d", g); TIME(l, (k_fill<1><<<g, 256>>>(buf, n)), n * 8.0, "GB/s");
+    snprintf(l, 64, "fill u64 v2 grid=%d", g); TIME(l, (k_fill<2><<<g, 256>>>(buf, n)), n * 8.0, "GB/s");
+    snprintf(l, 64, "fill u64 v4 grid=%d", g); TIME(l, (k_fill<4><<<g, 256>>>(buf, n)), n * 8.0, "GB/s");
+  }
+  TIME("cudaMemsetAsync 32GiB", (cudaMemsetAsync(buf, 0, n * 8)), n * 8.0, "GB/s");
+  printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
