@@ -71,6 +71,15 @@ def lib():
     """Load librs.so (building it if stale and nvcc is present)."""
     global _lib
     if _lib is None:
+        override = os.environ.get("RS_LIB")      # dev: benchmark a variant build
+        if override:
+            L = C.CDLL(override)
+            for name, (res, args) in SIGNATURES.items():
+                f = getattr(L, name)
+                f.restype = res
+                f.argtypes = args
+            _lib = L
+            return _lib
         if not os.path.exists(LIB_PATH) or _build.stale():
             try:
                 _build.build()

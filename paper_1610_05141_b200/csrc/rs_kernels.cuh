@@ -127,9 +127,15 @@ __global__ void __launch_bounds__(LEAF_NT) k_leaf_comp32(LeafArgs a);
 __global__ void __launch_bounds__(LEAF_NT) k_leaf_comp64(LeafArgs a);
 
 // Warp-per-leaf kernels (u32 keys): the common path; see rs_leaf.cuh.
-constexpr int WL_WARPS = 4;                      // warps (independent leaves) per CTA
-__global__ void __launch_bounds__(32 * WL_WARPS, 4) k_leaf_warp_wor(LeafArgs a);
-__global__ void __launch_bounds__(32 * WL_WARPS, 4) k_leaf_warp_wr(LeafArgs a);
+#ifndef RS_WL_MINB
+#define RS_WL_MINB 4
+#endif
+#ifndef RS_WL_WARPS
+#define RS_WL_WARPS 4
+#endif
+constexpr int WL_WARPS = RS_WL_WARPS;            // warps (independent leaves) per CTA
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor(LeafArgs a);
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr(LeafArgs a);
 
 // ---------------------------------------------------------------------------
 // Bernoulli (row a9): one chunk per CTA (dynamic ticket order), geometric
