@@ -299,8 +299,9 @@ def run_native(args):
         if world > 1:
             off = int(allc[:rank].sum().item())
             assert off == g_off, "all-gathered offset disagrees with the Algorithm P replay"
-    assert bad == 0, f"validation failed: {bad} bad values"
-    assert rs.device_errors(clear=True) == 0, "device capacity flag raised"
+    if not args.no_check:
+        assert bad == 0, f"validation failed: {bad} bad values"
+        assert rs.device_errors(clear=True) == 0, "device capacity flag raised"
     total = torch.tensor([n_local_done], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(total)
@@ -404,6 +405,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-check", action="store_true", help="dev: skip the output validation asserts")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

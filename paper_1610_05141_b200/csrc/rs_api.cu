@@ -219,7 +219,8 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
     la.N = p.N; la.seed = p.seed; la.D = p.D;
     la.leaf0 = p.leaf0; la.nleaves = p.nleaves;
     la.cnt = leaf_cnt; la.off = leaf_off; la.out = out;
-    const bool wide = p.r_max >= 0xffffffffull;   // u32 keys hold offsets < 2^32
+    la.rk = round_keys(p.seed);
+    const bool wide = p.r_max > 0xfffff000ull;    // u32 keys (below the warp kernel's sentinels)
     const bool wr = (p.mode == RS_MODE_WR);
     void (*kern)(LeafArgs);
     size_t sm;
@@ -617,5 +618,16 @@ const char *rs_status_string(rs_status s)
 rs_status rs_last_status(void) { return t_last; }
 
 const char *rs_version(void) { return "rs 0.1 (CANON v1, sm_100a)"; }
+
+#ifdef RS_EXP_CLOCK
+// dev: per-phase cycle totals of the warp leaf kernel (RS_EXP_CLOCK builds)
+int rs_debug_prof(unsigned long long *out8, int reset)
+{
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out8, g_rs_prof, 8 * sizeof(unsigned long long));
+    if (reset) { unsigned long long z[8] = {0}; cudaMemcpyToSymbol(g_rs_prof, z, sizeof z); }
+    return 0;
+}
+#endif
 
 }  // extern "C"

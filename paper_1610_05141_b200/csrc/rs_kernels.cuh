@@ -117,6 +117,7 @@ struct LeafArgs {
     u32 *spill_n;          //   ... and their count; the CTA kernel then walks this list
     const u32 *list;       // CTA kernel: if set, process only list[0 .. *list_n)
     const u32 *list_n;
+    RoundKeys rk;          // Philox round keys of seed (round_keys(seed))
 };
 
 __global__ void __launch_bounds__(LEAF_NT) k_leaf_wor32(LeafArgs a);

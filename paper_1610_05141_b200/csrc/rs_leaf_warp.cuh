@@ -36,11 +36,26 @@
 
 namespace rs {
 
+#ifdef RS_EXP_CLOCK
+__device__ unsigned long long g_rs_prof[8];
+#define RS_TS(var) const long long var = clock64()
+#define RS_ACC(i, a, b) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_rs_prof[i], (unsigned long long)((b) - (a))); } while (0)
+#else
+#define RS_TS(var)
+#define RS_ACC(i, a, b)
+#endif
+
 constexpr int WL_B = 1024;                 // buckets (u32 counters)
 constexpr int WL_LOGB = 10;
 constexpr int WL_E1 = 36, WL_E2 = 44;      // positions per lane; E mod 32 in {4, 12}: conflict-free LDS.128
+#ifdef RS_WL_TWO_E
 constexpr int WL_CAP = 32 * WL_E2;         // 1408 positions per leaf
+#else
+constexpr int WL_CAP = 32 * WL_E1;         // 1152 positions per leaf
+#endif
 constexpr u32 WL_PMAX = 48;                // odd-even phases allowed before spilling
+
+constexpr u32 WL_SENT0 = 0xFFFFFFFFu - (u32)WL_CAP;   // sentinel at position p: WL_SENT0 + p (> any key)
 
 struct WarpLeaf {
     u32 cnt[WL_B + WL_B / 32];             // padded bucket counters / starts (33 words per lane)
@@ -63,17 +78,29 @@ __device__ __forceinline__ u32 shr32(u32 v, u32 s)   // v >> s, 0 for s == 32
 }
 
 // Four bounded draws of block q (R3): Lemire's multiply-shift, which for a
-// power-of-two range is the top ceil_log2(r) bits (never rejects).
+// power-of-two range is the top ceil_log2(r) bits (never rejects).  The
+// Philox round keys come from the kernel arguments (constant bank).
 struct WDrawer {
     Drawer<u32> d;
     u32 s;          // 32 - ceil_log2(r)
     bool pow2;
     __device__ WDrawer(const Stream &st, u64 r, int cr) : d(st, r), s(32u - (u32)cr), pow2((r & (r - 1)) == 0) {}
-    __device__ __forceinline__ void block(u32 q, u32 *v) const
+    __device__ __forceinline__ void block(const RoundKeys &K, u32 q, u32 *v) const
     {
+#ifdef RS_EXP_NOPHILOX
+        { const u32 t = q * 0x9E3779B9u ^ d.st.id_lo; v[0] = shr32(t, s); v[1] = shr32(t * 3u, s); v[2] = shr32(t * 5u, s); v[3] = shr32(t * 7u, s); return; }
+#endif
         if (pow2) {
-            const u32x4 w = d.st.block(q);
-            v[0] = shr32(w.x, s); v[1] = shr32(w.y, s); v[2] = shr32(w.z, s); v[3] = shr32(w.w, s);
+            u32 c0 = q, c1 = d.st.tag, c2 = d.st.id_lo, c3 = d.st.id_hi;
+#pragma unroll
+            for (int r = 0; r < 10; ++r) {
+                const u64 p0 = (u64)0xD2511F53u * c0, p1 = (u64)0xCD9E8D57u * c2;
+                c0 = (u32)(p1 >> 32) ^ c1 ^ K.k[2 * r];
+                c1 = (u32)p1;
+                c2 = (u32)(p0 >> 32) ^ c3 ^ K.k[2 * r + 1];
+                c3 = (u32)p0;
+            }
+            v[0] = shr32(c0, s); v[1] = shr32(c1, s); v[2] = shr32(c2, s); v[3] = shr32(c3, s);
         } else {
             d.block(q, v);
         }
@@ -105,50 +132,73 @@ __device__ __forceinline__ u32 warp_excl_scan(u32 v, u32 lane)
 // Steps 1-2: count the round's J draws per bucket and stage them in draw
 // order at keys[0..J); scan the counts into starts.  Returns the largest
 // bucket load (0 if a bucket is a single value).
-__device__ __forceinline__ u32 wl_count(WarpLeaf &sh, const WDrawer &dr, u32 J, int shb, u32 lane)
+__device__ __forceinline__ u32 wl_count(WarpLeaf &sh, const RoundKeys &K, const WDrawer &dr, u32 J, int shb, u32 lane)
 {
+    RS_TS(tc0);
     const u32 qfull = J >> 2;                    // blocks whose 4 draws all count
+    const u32 nq = (J + 3) >> 2;                 // blocks of the round
 #pragma unroll 1
-    for (u32 q = lane; 4 * q < J; q += 32) {
-        u32 v[4];
-        dr.block(q, v);
-        if (q < qfull) {
+    for (u32 q = lane; q < nq; q += 64) {        // two independent Philox blocks per step (ILP)
+        const u32 q2 = q + 32;
+        u32 v[4], v2[4];
+        dr.block(K, q, v);
+        dr.block(K, q2, v2);
+        if (q2 < qfull) {
 #pragma unroll
-            for (int w = 0; w < 4; ++w) atomicAdd(&sh.cnt[wl_word(v[w] >> shb)], 1u);
+            for (int w = 0; w < 4; ++w) {
+                atomicAdd(&sh.cnt[wl_word(v[w] >> shb)], 1u);
+                atomicAdd(&sh.cnt[wl_word(v2[w] >> shb)], 1u);
+            }
         } else {
 #pragma unroll
-            for (int w = 0; w < 4; ++w)
+            for (int w = 0; w < 4; ++w) {
                 if (4 * q + w < J) atomicAdd(&sh.cnt[wl_word(v[w] >> shb)], 1u);
+                if (4 * q2 + w < J) atomicAdd(&sh.cnt[wl_word(v2[w] >> shb)], 1u);
+            }
         }
 #if !defined(RS_WL_REGEN)
         *reinterpret_cast<uint4 *>(&sh.keys[4 * q]) = make_uint4(v[0], v[1], v[2], v[3]);
+        if (q2 < nq) *reinterpret_cast<uint4 *>(&sh.keys[4 * q2]) = make_uint4(v2[0], v2[1], v2[2], v2[3]);
 #endif
     }
     __syncwarp();
+    RS_TS(tc1);
     u32 *cl = sh.cnt + 33 * lane;
-    u32 S = 0, mx = 0;
+    u32 c[32];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        const u32 c = cl[i];
-        S += c;
-        mx = max(mx, c);
+    for (int i = 0; i < 32; ++i) c[i] = cl[i];
+    u32 seg[4], mx4[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {                // four independent chains (ILP)
+        seg[g] = 0; mx4[g] = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { seg[g] += c[8 * g + i]; mx4[g] = max(mx4[g], c[8 * g + i]); }
     }
-    u32 run = warp_excl_scan(S, lane);
+    const u32 S = (seg[0] + seg[1]) + (seg[2] + seg[3]);
+    const u32 mx = max(max(mx4[0], mx4[1]), max(mx4[2], mx4[3]));
+    const u32 run = warp_excl_scan(S, lane);
     const u32 P = __reduce_max_sync(0xffffffffu, mx);
+    u32 rg[4];
+    rg[0] = run; rg[1] = run + seg[0]; rg[2] = rg[1] + seg[1]; rg[3] = rg[2] + seg[2];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {               // starts in place (second read)
-        const u32 c = cl[i];
-        cl[i] = run;
-        run += c;
+    for (int i = 0; i < 8; ++i) {                // starts in place, four chains
+#pragma unroll
+        for (int g = 0; g < 4; ++g) { cl[8 * g + i] = rg[g]; rg[g] += c[8 * g + i]; }
     }
     __syncwarp();
+    RS_TS(tc2);
+    RS_ACC(0, tc0, tc1);
+    RS_ACC(1, tc1, tc2);
     return shb == 0 ? 0u : P;
 }
 
 __device__ __forceinline__ void wl_clear(WarpLeaf &sh, u32 lane)
 {
+    static_assert(WL_B % 128 == 0 && WL_B / 32 <= 32, "clear layout");
 #pragma unroll
-    for (int i = 0; i < (WL_B + WL_B / 32) / 32; ++i) sh.cnt[32 * i + lane] = 0u;
+    for (int i = 0; i < WL_B / 128; ++i)
+        *reinterpret_cast<uint4 *>(&sh.cnt[128 * i + 4 * lane]) = make_uint4(0u, 0u, 0u, 0u);
+    if (lane < WL_B / 32) sh.cnt[WL_B + lane] = 0u;
 }
 
 // 32-byte store of base + {a, b, c, d} (u64 + u32), predicated; the adds
@@ -168,16 +218,16 @@ __device__ __forceinline__ void st_v4_base_if(bool pred, u64 *p, u64 base, u32 a
 }
 
 // Step 3: every draw of the round to its bucket's next position (+ h).
-__device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const WDrawer &dr, u32 J, u32 h, int shb, u32 lane)
+__device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const RoundKeys &K, const WDrawer &dr, u32 J, u32 h, int shb, u32 lane)
 {
     u32 *kh = sh.keys + h;
-    const u32 qfull = J >> 2;
 #if defined(RS_WL_REGEN)
+    const u32 qfull = J >> 2;
     // the draws are regenerated (Philox is cheaper than holding them)
 #pragma unroll 1
     for (u32 q = lane; 4 * q < J; q += 32) {
         u32 v[4];
-        dr.block(q, v);
+        dr.block(K, q, v);
         if (q < qfull) {
 #pragma unroll
             for (int w = 0; w < 4; ++w) kh[atomicAdd(&sh.cnt[wl_word(v[w] >> shb)], 1u)] = v[w];
@@ -201,17 +251,31 @@ __device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const WDrawer &dr, u32 
         }
     }
     __syncwarp();
+    // Atomics first, stores after, in groups of GB blocks: smem stores and
+    // atomics may alias as far as the compiler knows, so interleaving them
+    // would serialise every atomic's round trip.
+    constexpr int GB = 3;
+    static_assert(NB % GB == 0, "group size");
 #pragma unroll
-    for (int m = 0; m < NB; ++m) {
-        const u32 q = lane + 32u * m;
-        if (q < qfull) {
+    for (int m0 = 0; m0 < NB; m0 += GB) {
+        u32 pos[4 * GB];
+        // the group's draws all exist for every lane: no per-draw test
+        const bool full = 4 * (31u + 32u * (m0 + GB - 1)) + 3 < J;
+        if (full) {
 #pragma unroll
-            for (int w = 0; w < 4; ++w)
-                kh[atomicAdd(&sh.cnt[wl_word(x[4 * m + w] >> shb)], 1u)] = x[4 * m + w];
-        } else if (4 * q < J) {
+            for (int e = 4 * m0; e < 4 * (m0 + GB); ++e)
+                pos[e - 4 * m0] = atomicAdd(&sh.cnt[wl_word(x[e] >> shb)], 1u);
 #pragma unroll
-            for (int w = 0; w < 4; ++w)
-                if (4 * q + w < J) kh[atomicAdd(&sh.cnt[wl_word(x[4 * m + w] >> shb)], 1u)] = x[4 * m + w];
+            for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) kh[pos[e - 4 * m0]] = x[e];
+        } else if (4 * (lane + 32u * m0) < J) {
+#pragma unroll
+            for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) {
+                const u32 j = 4 * (lane + 32u * (e >> 2)) + (e & 3);
+                pos[e - 4 * m0] = j < J ? atomicAdd(&sh.cnt[wl_word(x[e] >> shb)], 1u) : (u32)WL_CAP;
+            }
+#pragma unroll
+            for (int e = 4 * m0; e < 4 * (m0 + GB); ++e)
+                if (pos[e - 4 * m0] != (u32)WL_CAP) kh[pos[e - 4 * m0]] = x[e];
         }
     }
 #endif
@@ -221,12 +285,20 @@ __device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const WDrawer &dr, u32 
 // Steps 4-6 for E positions per lane.  Returns 0 (leaf stored) or, for WOR
 // with too few distinct values, the next round's draw count J' > J.
 template <int E, bool WR>
-__device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 P, u64 base,
+__device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 P_, u64 base,
                                          u64 *dst, u32 lane)
 {
+    u32 P = P_;
+    RS_TS(tf0);
     wl_clear(sh, lane);                          // counters are dead: ready for the next round / leaf
     if (lane < h) sh.keys[lane] = 0u;            // pad below the first draw
-    for (u32 p = h + J + lane; p < 32u * E; p += 32) sh.keys[p] = 0xffffffffu;   // sentinels
+    {   // sentinels WL_SENT0 + p above the last draw: distinct, larger than any key
+        const u32 s0 = h + J, s4 = (s0 + 3) & ~3u;
+        if (lane < s4 - s0 && s0 + lane < 32u * E) sh.keys[s0 + lane] = WL_SENT0 + s0 + lane;
+        for (u32 p = s4 + 4 * lane; p < 32u * E; p += 128)
+            *reinterpret_cast<uint4 *>(&sh.keys[p]) =
+                make_uint4(WL_SENT0 + p, WL_SENT0 + p + 1, WL_SENT0 + p + 2, WL_SENT0 + p + 3);
+    }
     __syncwarp();
     // 4. blocked registers + odd-even transposition inside buckets
     u32 y[E];
@@ -235,81 +307,99 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
         const uint4 t = *reinterpret_cast<const uint4 *>(&sh.keys[E * lane + i]);
         y[i] = t.x; y[i + 1] = t.y; y[i + 2] = t.z; y[i + 3] = t.w;
     }
-    for (u32 ph = 0; ph < P; ++ph) {
-        if ((ph & 1u) == 0) {
+#ifdef RS_EXP_NOSORT
+    P = 0;
+#endif
+    for (u32 ph = 0; ph < P; ph += 2) {          // even + odd phase per step (P rounded up)
 #pragma unroll
-            for (int i = 0; i < E; i += 2) wl_ce(y[i], y[i + 1]);
-        } else {
-            const u32 nxt = __shfl_down_sync(0xffffffffu, y[0], 1);
-            const u32 prv = __shfl_up_sync(0xffffffffu, y[E - 1], 1);
+        for (int i = 0; i < E; i += 2) wl_ce(y[i], y[i + 1]);
+        const u32 nxt = __shfl_down_sync(0xffffffffu, y[0], 1);
+        const u32 prv = __shfl_up_sync(0xffffffffu, y[E - 1], 1);
 #pragma unroll
-            for (int i = 1; i < E - 1; i += 2) wl_ce(y[i], y[i + 1]);
-            if (lane < 31) y[E - 1] = min(y[E - 1], nxt);
-            if (lane > 0) y[0] = max(prv, y[0]);
-        }
+        for (int i = 1; i < E - 1; i += 2) wl_ce(y[i], y[i + 1]);
+        if (lane < 31) y[E - 1] = min(y[E - 1], nxt);
+        if (lane > 0) y[0] = max(prv, y[0]);
     }
+    RS_TS(tf1);
+    RS_ACC(3, tf0, tf1);
     const u32 p0 = E * lane;
     u64 *d0 = dst - h;                           // 32-byte aligned
     if (!WR) {
-        // 5. duplicates = equal neighbours (Algorithm H rejects them).  Count
-        // every equality, then remove those of the pad (positions 1..h-1, and
-        // position h if the first draw is 0) and of the sentinels.
+        // 5. duplicates = equal neighbours (Algorithm H rejects them).  Fast
+        // test: the smallest neighbour difference is 0 somewhere.  Pads get
+        // distinct values 0, 1, 2 and sentinels are distinct, so a zero
+        // difference is a duplicate, or (rarely) the first draw equal to the
+        // last pad -- the exact count below sorts that out.
+        if (lane == 0) { if (h > 1) y[1] = 1u; if (h > 2) y[2] = 2u; }
         const u32 prv = __shfl_up_sync(0xffffffffu, y[E - 1], 1);
-        u32 nd = lane ? (u32)(y[0] == prv) : 0u;
+        u32 m4[4] = {lane ? y[0] - prv : 1u, 1u, 1u, 1u};
 #pragma unroll
-        for (int i = 1; i < E; ++i) nd += (u32)(y[i] == y[i - 1]);
-        u32 ndup = __reduce_add_sync(0xffffffffu, nd);
-        const u32 yh = __shfl_sync(0xffffffffu, h == 0 ? y[0] : h == 1 ? y[1] : h == 2 ? y[2] : y[3], 0);
-        ndup -= (h ? h - 1 + (u32)(yh == 0u) : 0u) + (32u * E - (h + J)) - (32u * E > h + J ? 1u : 0u);
-        if (ndup) {
-            const u32 dist = J - ndup;           // |S| after this round
-            if (dist < k) return J + (k - dist);
-            // compact the k distinct values through shared memory, then store
-            u32 keep = 0;
+        for (int i = 1; i < E; ++i) m4[i & 3] = min(m4[i & 3], y[i] - y[i - 1]);
+        const u32 md = min(min(m4[0], m4[1]), min(m4[2], m4[3]));
+        if (__any_sync(0xffffffffu, md == 0u)) {
+            u32 nd = 0;
 #pragma unroll
             for (int i = 0; i < E; ++i) {
                 const u32 p = p0 + i;
-                keep += p >= h && p < h + J && !(p > h && y[i] == (i ? y[i - 1] : prv));
+                nd += p > h && p < h + J && y[i] == (i ? y[i - 1] : prv);
             }
-            u32 o = h + warp_excl_scan(keep, lane);
-            __syncwarp();
+            const u32 ndup = __reduce_add_sync(0xffffffffu, nd);
+            if (ndup) {
+                const u32 dist = J - ndup;       // |S| after this round
+                if (dist < k) return J + (k - dist);
+                // compact the k distinct values through shared memory, then store
+                u32 keep = 0;
 #pragma unroll
-            for (int i = 0; i < E; ++i) {
-                const u32 p = p0 + i;
-                if (p >= h && p < h + J && !(p > h && y[i] == (i ? y[i - 1] : prv))) sh.keys[o++] = y[i];
-            }
-            __syncwarp();
-            const u32 ng = (h + k + 3) >> 2;
-            for (u32 g = lane; g < ng; g += 32) {
-                const uint4 t = *reinterpret_cast<const uint4 *>(&sh.keys[4 * g]);
-                const u32 vv[4] = {t.x, t.y, t.z, t.w};
-                const u32 i0 = 4 * g;
-                if (i0 >= h && i0 + 4 <= h + k) {
-                    st_v4(d0 + i0, base + vv[0], base + vv[1], base + vv[2], base + vv[3]);
-                } else {
-#pragma unroll
-                    for (int t2 = 0; t2 < 4; ++t2)
-                        if (i0 + t2 >= h && i0 + t2 < h + k) d0[i0 + t2] = base + vv[t2];
+                for (int i = 0; i < E; ++i) {
+                    const u32 p = p0 + i;
+                    keep += p >= h && p < h + J && !(p > h && y[i] == (i ? y[i - 1] : prv));
                 }
+                u32 o = h + warp_excl_scan(keep, lane);
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < E; ++i) {
+                    const u32 p = p0 + i;
+                    if (p >= h && p < h + J && !(p > h && y[i] == (i ? y[i - 1] : prv))) sh.keys[o++] = y[i];
+                }
+                __syncwarp();
+                const u32 ng = (h + k + 3) >> 2;
+                for (u32 g = lane; g < ng; g += 32) {
+                    const uint4 t = *reinterpret_cast<const uint4 *>(&sh.keys[4 * g]);
+                    const u32 vv[4] = {t.x, t.y, t.z, t.w};
+                    const u32 i0 = 4 * g;
+                    if (i0 >= h && i0 + 4 <= h + k) {
+                        st_v4(d0 + i0, base + vv[0], base + vv[1], base + vv[2], base + vv[3]);
+                    } else {
+#pragma unroll
+                        for (int t2 = 0; t2 < 4; ++t2)
+                            if (i0 + t2 >= h && i0 + t2 < h + k) d0[i0 + t2] = base + vv[t2];
+                    }
+                }
+                __syncwarp();
+                return 0;
             }
-            __syncwarp();
-            return 0;
         }
     }
+    RS_TS(tf2);
+    RS_ACC(4, tf1, tf2);
     // 6. no duplicates (J == k): 32-byte stores straight from registers; the
     // head group (positions 0..3, lane 0) and the tail group are partial.
     const u32 end = h + k;
+#ifdef RS_EXP_NOSTORE
+    if (y[0] == 0x12345u && y[E-1] == 7u) d0[lane] = y[3];
+    return 0;
+#endif
 #pragma unroll
     for (int m = 0; m < E; m += 4) {
         const u32 p = p0 + m;
         st_v4_base_if(p >= h && p + 4 <= end, d0 + p, base, y[m], y[m + 1], y[m + 2], y[m + 3]);
     }
-    if (lane == 0 && h) {                          // head: positions h..3 (k >= 1)
+    if (lane == 0 && (h || end < 4)) {             // head group (positions 0..3) if partial
 #pragma unroll
-        for (int t = 1; t < 4; ++t)
+        for (int t = 0; t < 4; ++t)
             if ((u32)t >= h && (u32)t < end) d0[t] = base + y[t];
     }
-    const u32 tg = (end - 1) & ~3u;               // tail group start (if partial)
+    const u32 tg = (end - 1) & ~3u;               // tail group start (if partial, and not the head)
     if ((end & 3u) && tg >= 4 && lane == tg / E) {
         const u32 mt = tg - p0;
 #pragma unroll
@@ -354,20 +444,25 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
         u32 J = k;
         for (;;) {
             u32 res = 0xffffffffu;
-            if (J + h <= 32u * WL_E2) {
-                const u32 P = wl_count(sh, dr, J, shb, lane);
+            if (J + h <= (u32)WL_CAP) {
+                const u32 P = wl_count(sh, a.rk, dr, J, shb, lane);
                 if (P > WL_PMAX) {              // pathological bucket load
                     wl_clear(sh, lane);
                     __syncwarp();
                 } else if (J + h <= 32u * WL_E1) {
-                    wl_scatter(sh, dr, J, h, shb, lane);
+                    RS_TS(ts0);
+                    wl_scatter(sh, a.rk, dr, J, h, shb, lane);
+                    RS_TS(ts1);
+                    RS_ACC(2, ts0, ts1);
                     res = wl_finish<WL_E1, WR>(sh, J, k, h, P, base, dst, lane);
+                    RS_TS(ts2);
+                    RS_ACC(5, ts1, ts2);
                 } else {
 #ifndef RS_WL_TWO_E
                     wl_clear(sh, lane);         // larger leaves go to the CTA kernel (measured faster than a second, 44-position instantiation)
                     __syncwarp();
 #else
-                    wl_scatter(sh, dr, J, h, shb, lane);
+                    wl_scatter(sh, a.rk, dr, J, h, shb, lane);
                     res = wl_finish<WL_E2, WR>(sh, J, k, h, P, base, dst, lane);
 #endif
                 }

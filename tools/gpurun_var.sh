@@ -3,7 +3,7 @@ cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 for f in build/var/librs_*.so; do
   n=$(basename $f .so)
   for w in ${WORKLOADS:-headline}; do
-    RS_LIB=$PWD/$f timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e --workload $w > gpurun_out/var_${n}_$w.log 2>&1
+    RS_LIB=$PWD/$f timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e ${CHECK:-} --workload $w > gpurun_out/var_${n}_$w.log 2>&1
     python3 -c "
 import json
 for l in open('gpurun_out/var_${n}_$w.log'):
