@@ -224,7 +224,17 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
     const bool wr = (p.mode == RS_MODE_WR);
     void (*kern)(LeafArgs);
     size_t sm;
-    if (p.comp) {
+    if (p.r_max <= BM_RMAX && p.mode == RS_MODE_WOR) {
+        // small leaf ranges: warp per leaf over a bitmap (complement or WOR)
+        la.out_base = p.shard_lo;
+        void (*bk)(LeafArgs) = p.comp ? k_leaf_bitmap_comp : k_leaf_bitmap_wor;
+        const size_t bsm = sizeof(BitmapLeaf) * WL_WARPS;
+        const unsigned gb = leaf_grid((const void *)bk, 32 * WL_WARPS, bsm, (p.nleaves + WL_WARPS - 1) / WL_WARPS);
+        bk<<<gb, 32 * WL_WARPS, bsm, st>>>(la);
+        ++t_launches;
+        sp_leaf.end();
+        return cuda_ok();
+    } else if (p.comp) {
         la.out_base = p.shard_lo;
         la.tiles_per_leaf = (p.r_max + COMP_TILE - 1) / COMP_TILE;
         kern = wide ? k_leaf_comp64 : k_leaf_comp32;

@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(LEVEL_NT, 8) k_split_level(LevelArgs a)
 
 #include "rs_leaf.cuh"
 #include "rs_leaf_warp.cuh"
+#include "rs_leaf_bitmap.cuh"
 
 namespace rs {
 

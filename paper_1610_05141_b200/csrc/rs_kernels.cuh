@@ -137,6 +137,9 @@ __global__ void __launch_bounds__(LEAF_NT) k_leaf_comp64(LeafArgs a);
 constexpr int WL_WARPS = RS_WL_WARPS;            // warps (independent leaves) per CTA
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr(LeafArgs a);
+// Warp-per-leaf bitmap kernels for leaf ranges r <= 2^15 (rs_leaf_bitmap.cuh).
+__global__ void __launch_bounds__(32 * WL_WARPS) k_leaf_bitmap_wor(LeafArgs a);
+__global__ void __launch_bounds__(32 * WL_WARPS) k_leaf_bitmap_comp(LeafArgs a);
 
 // ---------------------------------------------------------------------------
 // Bernoulli (row a9): one chunk per CTA (dynamic ticket order), geometric
