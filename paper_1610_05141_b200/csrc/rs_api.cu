@@ -375,8 +375,19 @@ rs_status bern_call(u64 N, double rho, u64 seed, int world, int rank, u64 *out, 
     a.status = (u64 *)(w + p.o_status);
     a.ticket = (u32 *)(w + p.o_ticket);
     a.out = out; a.capacity = capacity; a.count_dev = count_dev;
+    a.rk = round_keys(seed);
     Span sp(2, cs);
-    k_bernoulli<<<(unsigned)p.nchunks, BERN_NT, 0, cs>>>(a);
+    {
+        const u64 rmax = (N >> p.Db) + 1;
+        void (*bk)(BernArgs) = rmax <= (1ull << 16) ? k_bernoulli : rmax <= (1ull << 24) ? k_bernoulli32 : k_bernoulli64;
+        int per = 0, dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(bk, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk, 128, 0) != cudaSuccess || per < 1) per = 1;
+        const u64 need = (p.nchunks + 3) / 4, g = (u64)sms * per;   // (over-provisioned: tickets end the loop)
+        bk<<<(unsigned)(need < g ? need : g), 128, 0, cs>>>(a);
+    }
     sp.end();
     ++t_launches;
     st = cuda_ok();

@@ -86,86 +86,207 @@ namespace rs {
 
 // ===========================================================================
 // Bernoulli (a9): dyadic chunks, geometric skips G = floor(log U/log1p(-rho))
-// (P:199-201), chunk-local chain restarted at chunk starts ("independently
-// apply Bernoulli sampling to subranges").  Each batch of
-// 2*BERN_NT skips is prefix-summed in one block scan (the paper's
-// "prefix sums of geometric deviates", without materialising them);
-// chunk offsets come from a single-pass decoupled look-back.
+// (P:199-201), the chain restarted at each chunk start ("independently apply
+// Bernoulli sampling to subranges").  ONE WARP PER CHUNK: each
+// step a lane turns one Philox block into two skips, and a warp scan of the
+// steps G+1 gives 64 consecutive positions (the paper's "prefix sums of
+// geometric deviates", without materialising them).  Positions go
+// to a shared-memory buffer; the chunk's output offset comes from a
+// single-pass decoupled look-back over chunk counts (lane-parallel), then the
+// buffer is stored coalesced.
+//
+// G in fp32 first, CERTIFIED: q' = log2(U') * (ln 2 / lr) with U' = U rounded
+// to fp32 and log2 by MUFU; |q' - q| is bounded (U' relative error 2^-24,
+// __log2f absolute error <= 2^-22.6 on [0.5, 2] and <= 2 ulp elsewhere, two
+// fp32 roundings) far below the margin used here; when [q' - margin,
+// q' + margin] contains no integer, floor(q') == floor(q) and that is G;
+// otherwise (about 1 draw in 2000 at rho = 0.01) G is evaluated exactly in
+// fp64 as CANON defines it (log_, IEEE division, floor).  Bit-exact either way.
 // ===========================================================================
-__device__ __forceinline__ u64 skip_step(double U, double lr, u64 r)
+template <typename T>
+__device__ __forceinline__ T skip_exact(double U, double lr, T r)
 {
     const double G = floor_(log_(U) / lr);
-    return G >= (double)r ? r + 1 : (u64)G + 1;   // any G >= r ends the chain
+    return G >= (double)r ? r + 1 : (T)G + 1;       // any G >= r ends the chain
 }
 
-__global__ void __launch_bounds__(BERN_NT) k_bernoulli(BernArgs a)
+// fp32 candidate for G (see above): sets ok when floor is certain; the
+// result saturates at r (any G >= r ends the chain).  Branch-free.
+__device__ __forceinline__ u32 skip_fast(u32 a, u32 b, float c, float m_abs, u32 r, bool &ok)
 {
-    __shared__ u64 vals[BERN_CAP];
-    __shared__ u64 wtmp[BERN_NT / 32];
-    __shared__ u64 tot;
-    __shared__ u64 s_chunk, s_excl;
-    const int tid = threadIdx.x;
-    if (tid == 0) s_chunk = atomicAdd(a.ticket, 1u);
-    __syncthreads();
-    const u64 c = s_chunk;
-    const u64 gi = a.chunk0 + c;
-    const u64 lo = bound_at(a.N, a.Db, gi);
-    const u64 r = bound_at(a.N, a.Db, gi + 1) - lo;
-    const Stream st(a.seed, P_GEO, ((u64)1 << a.Db) + gi);
-    u64 S = 0;          // sum of steps before this batch
-    u32 count = 0;
-    bool overflow = false;
-    for (u64 batch = 0;; ++batch) {
-        const u64 q = batch * BERN_NT + tid;            // Philox block: draws 2q, 2q+1
-        const u32x4 w = st.block((u32)q);
-        const u64 s0 = skip_step(u52(w.x, w.y), a.log1m_rho, r);
-        const u64 s1 = skip_step(u52(w.z, w.w), a.log1m_rho, r);
-        const u64 pre = block_exclusive_scan<u64, BERN_NT>(s0 + s1, wtmp, &tot);
-        const u64 S0 = S + pre + s0, S1 = S0 + s1;     // positions: lo + S - 1
-        const u32 e0 = S0 <= r, e1 = S1 <= r;
-        const u32 slot = count + 2 * tid;
-        if (e0) { if (slot < BERN_CAP) vals[slot] = lo + S0; else overflow = true; }
-        if (e1) { if (slot + 1 < BERN_CAP) vals[slot + 1] = lo + S1; else overflow = true; }
-        const u32 emitted = __syncthreads_count(e0) + __syncthreads_count(e1);
-        count += emitted;
-        S += tot;
-        if (emitted < 2u * BERN_NT) break;
-        __syncthreads();
-    }
-    if (__syncthreads_or(overflow)) {
-        if (tid == 0) atomicOr(&g_rs_errors, 2u);
-        count = count < BERN_CAP ? count : BERN_CAP;
-    }
-    // decoupled look-back: flag bits 63:62 = 1 aggregate, 2 inclusive prefix
+    const u64 m = ((((u64)a << 32) | b) >> 11) | 1ull;              // 2 * (u52 mantissa) + 1
+    const float U = __ull2float_rn(m) * 0x1p-53f;                   // U rounded to fp32
+    const float q = __log2f(U) * c;                                 // ~ log(U) / lr  (> 0)
+    const float mg = m_abs + q * 0x1p-20f;
+    const float lo = floorf(q - mg), hi = floorf(q + mg);
+    const float rf = (float)r;
+    ok = lo >= rf || (lo == hi && lo >= 0.0f);
+    return lo >= rf ? r : (u32)fminf(lo, rf);
+}
+
+__device__ __forceinline__ void st_relaxed(u64 *p, u64 v)
+{
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ u64 ld_relaxed(const u64 *p)
+{
+    u64 v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+constexpr int BW_WARPS = 4;
+// positions buffered per chunk (mean <= n0 = 1024; u64 positions only for
+// chunk ranges above 2^24, where the buffer is smaller to fit 48 KB)
+// A warp takes a TICKET of G consecutive chunks (fewer look-back
+// participants, and look-back waits amortised over G chunks), buffers their
+// positions (type B, relative to each chunk start) in shared memory, looks
+// back over tickets, then stores.  T = position arithmetic (u32 while a
+// batch's 64 steps fit, else u64).
+template <typename T, typename B, int G, u32 CAP>
+__device__ __forceinline__ void bernoulli_chunks(const BernArgs &a)
+{
+    __shared__ B buf[BW_WARPS][CAP];
+    const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    B *bw = buf[wid];
+    const float c = (float)(0x1.62e42fefa39efp-1 / a.log1m_rho);   // ln 2 / lr
+    const float m_abs = (float)(0x1p-19 / -a.log1m_rho) + 0x1p-20f;
     const u64 AGG = 1ull << 62, INC = 2ull << 62, VAL = (1ull << 62) - 1;
-    if (tid == 0) {
-        volatile u64 *stat = a.status;
-        u64 excl = 0;
-        if (c == 0) {
-            __threadfence();
-            stat[0] = INC | count;
-        } else {
-            stat[c] = AGG | count;
-            __threadfence();
-            for (u64 p = c - 1;; --p) {
-                u64 wv;
-                do { wv = stat[p]; } while ((wv >> 62) == 0);
-                excl += wv & VAL;
-                if ((wv >> 62) == 2) break;
+    const u64 ntick = (a.nchunks + G - 1) / G;
+    for (;;) {
+        u32 tk = 0;
+        if (lane == 0) tk = atomicAdd(a.ticket, 1u);
+        tk = __shfl_sync(0xffffffffu, tk, 0);
+        if (tk >= ntick) break;
+        u32 cnt[G];
+        u32 total = 0;
+        bool overflow = false;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            cnt[g] = 0;
+            const u64 ci = (u64)tk * G + g;
+            if (ci >= a.nchunks) continue;
+            const u64 gi = a.chunk0 + ci;
+            const u64 lo = bound_at(a.N, a.Db, gi);
+            const T r = (T)(bound_at(a.N, a.Db, gi + 1) - lo);
+            const u32 r32 = r > (T)0x7fffffffu ? 0x7fffffffu : (u32)r;    // fast path saturation point
+            const Stream st(a.seed, P_GEO, ((u64)1 << a.Db) + gi);
+            B *bg = bw + total;
+            const u32 room = CAP - total;
+            // skips in batches of 64 draws: lane l has draws 2(q0 + l), 2(q0 + l) + 1
+            T S = 0;
+            u32 count = 0;
+            for (u32 q0 = 0;; q0 += 32) {
+                const u32x4 w = philox_rk(q0 + lane, st, a.rk);
+                bool ok0, ok1;
+                const u32 g0 = skip_fast(w.x, w.y, c, m_abs, r32, ok0);
+                const u32 g1 = skip_fast(w.z, w.w, c, m_abs, r32, ok1);
+                T s0 = (T)g0 + 1, s1 = (T)g1 + 1;
+                if (__any_sync(0xffffffffu, !(ok0 && ok1))) {  // rare: exact fp64 (CANON)
+                    if (!ok0) s0 = skip_exact<T>(u52(w.x, w.y), a.log1m_rho, r);
+                    if (!ok1) s1 = skip_exact<T>(u52(w.z, w.w), a.log1m_rho, r);
+                }
+                T incl = s0 + s1;                              // inclusive scan over lanes
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const T y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= (u32)o) incl += y;
+                }
+                const T S1 = S + incl, S0 = S1 - s1;           // positions (relative) + 1
+                const u32 j0 = 2 * (q0 + lane);
+                if (S0 <= r) { if (j0 < room) bg[j0] = (B)(S0 - 1); else overflow = true; }
+                if (S1 <= r) { if (j0 + 1 < room) bg[j0 + 1] = (B)(S1 - 1); else overflow = true; }
+                const T tot = __shfl_sync(0xffffffffu, incl, 31);
+                const u32 e = __popc(__ballot_sync(0xffffffffu, S0 <= r)) +
+                              __popc(__ballot_sync(0xffffffffu, S1 <= r));
+                count += e;
+                if (e < 64) break;
+                S += tot;
             }
-            __threadfence();
-            stat[c] = INC | (excl + count);
+            if (__any_sync(0xffffffffu, overflow)) count = min(count, room);
+            cnt[g] = count;
+            total += count;
         }
-        s_excl = excl;
-        if (c == a.nchunks - 1) *a.count_dev = excl + count;
-    }
-    __syncthreads();
-    const u64 excl = s_excl;
-    for (u32 i = tid; i < count; i += BERN_NT) {
-        const u64 gpos = excl + i;
-        if (gpos < a.capacity) a.out[gpos] = vals[i];
+        if (__any_sync(0xffffffffu, overflow) && lane == 0) atomicOr(&g_rs_errors, 2u);
+        // decoupled look-back over tickets: status words (flag << 62 | value),
+        // relaxed gpu-scope accesses (each word carries its own value).  A lane
+        // reads four predecessors (128 per step); only predecessors nearer
+        // than the nearest inclusive one need to be published.
+        u64 excl = 0;
+#ifdef RS_EXP_NOLOOKBACK
+        excl = (u64)tk * G * 600;
+        if (true) {
+        } else
+#endif
+        if (tk == 0) {
+            if (lane == 0) st_relaxed(a.status, INC | total);
+        } else {
+            if (lane == 0) st_relaxed(a.status + tk, AGG | total);
+            long long p = (long long)tk - 1;
+            u64 v[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const long long idx = p - (long long)(4 * lane + t);
+                v[t] = idx >= 0 ? ld_relaxed(a.status + idx) : (INC | 0ull);
+            }
+            for (;;) {
+                u32 dinc = 0xffffffffu, dpen = 0xffffffffu;
+#pragma unroll
+                for (int t = 3; t >= 0; --t) {
+                    if ((v[t] >> 62) == 2) dinc = 4 * lane + t;
+                    if ((v[t] >> 62) == 0) dpen = 4 * lane + t;
+                }
+                dinc = __reduce_min_sync(0xffffffffu, dinc);
+                dpen = __reduce_min_sync(0xffffffffu, dpen);
+                if (dpen < dinc) {                          // a nearer predecessor is not published yet
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const long long idx = p - (long long)(4 * lane + t);
+                        if ((v[t] >> 62) == 0 && 4 * lane + t < dinc) v[t] = ld_relaxed(a.status + idx);
+                    }
+                    continue;
+                }
+                u64 add = 0;
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (4 * lane + t <= dinc) add += v[t] & VAL;   // dinc = ~0: all 128
+#pragma unroll
+                for (int o = 16; o; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+                excl += add;
+                if (dinc != 0xffffffffu) break;
+                p -= 128;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const long long idx = p - (long long)(4 * lane + t);
+                    v[t] = idx >= 0 ? ld_relaxed(a.status + idx) : (INC | 0ull);
+                }
+            }
+            if (lane == 0) st_relaxed(a.status + tk, INC | (excl + total));
+        }
+        if (lane == 0 && tk == ntick - 1) *a.count_dev = excl + total;
+        __syncwarp();
+        u32 off = 0;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const u64 ci = (u64)tk * G + g;
+            if (ci >= a.nchunks) break;
+            const u64 base = bound_at(a.N, a.Db, a.chunk0 + ci) + 1;
+            u64 *o = a.out + excl + off;
+            const u64 cap = a.capacity > excl + off ? a.capacity - (excl + off) : 0;
+            for (u32 i = lane; i < cnt[g]; i += 32)
+                if (i < cap) o[i] = base + (u64)bw[off + i];
+            off += cnt[g];
+        }
+        __syncwarp();
     }
 }
+
+// chunk range r <= 2^16: u16 positions, 4 chunks per ticket (4864 x 2 B per warp)
+__global__ void __launch_bounds__(32 * BW_WARPS) k_bernoulli(BernArgs a) { bernoulli_chunks<u32, uint16_t, 4, 4864>(a); }
+// r <= 2^24: u32 positions, 2 chunks per ticket (2560 x 4 B per warp)
+__global__ void __launch_bounds__(32 * BW_WARPS) k_bernoulli32(BernArgs a) { bernoulli_chunks<u32, u32, 2, 2560>(a); }
+// larger r: u64 positions, 1 chunk per ticket (1536 x 8 B per warp)
+__global__ void __launch_bounds__(32 * BW_WARPS) k_bernoulli64(BernArgs a) { bernoulli_chunks<u64, u64, 1, 1536>(a); }
 
 // ===========================================================================
 // Validation helpers.

@@ -145,8 +145,6 @@ __global__ void __launch_bounds__(32 * WL_WARPS) k_leaf_bitmap_comp(LeafArgs a);
 // Bernoulli (row a9): one chunk per CTA (dynamic ticket order), geometric
 // skips + block scan, decoupled look-back over chunk counts, store.
 // ---------------------------------------------------------------------------
-constexpr int BERN_NT = 256;
-constexpr int BERN_CAP = 4096;          // outputs held on chip per chunk
 
 struct BernArgs {
     u64 N, seed;
@@ -158,9 +156,12 @@ struct BernArgs {
     u64 *out;
     u64 capacity;
     u64 *count_dev;
+    RoundKeys rk;          // Philox round keys of seed
 };
 
-__global__ void __launch_bounds__(BERN_NT) k_bernoulli(BernArgs a);
+__global__ void __launch_bounds__(128) k_bernoulli(BernArgs a);     // chunk ranges <= 2^16
+__global__ void __launch_bounds__(128) k_bernoulli32(BernArgs a);   // chunk ranges <= 2^24
+__global__ void __launch_bounds__(128) k_bernoulli64(BernArgs a);   // larger chunk ranges
 
 // Validation (tests / bench correctness checks).
 __global__ void k_digest(const u64 *v, u64 n, u64 base, u64 *acc);
