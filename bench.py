@@ -322,8 +322,12 @@ def run_native(args):
         D = rs.plan(m, N, n)[0]
         nleaves = (1 << D) // world
         bytes_per_launch = 8.0 * n_local + 12.0 * nleaves
-        kname = "k_leaf_comp32" if (mode == "wor" and rs.plan(m, N, n)[1]) else (
-            "k_leaf_wr32" if mode == "wr" else "k_leaf_wor32")
+        comp = bool(rs.plan(m, N, n)[1])
+        r_max = (N >> D) + 1
+        if mode == "wor" and r_max <= 2 ** 15:
+            kname = "k_leaf_bitmap_comp" if comp else "k_leaf_bitmap_wor"
+        else:
+            kname = "k_leaf_warp_wr" if mode == "wr" else "k_leaf_warp_wor"
     kms_per = kms / max(kl, 1)
     achieved = bytes_per_launch / (kms_per / 1e3) / 1e9 if kms_per > 0 else None
     traffic = None

@@ -139,6 +139,14 @@ rs_status rs_plan(int mode, uint64_t N, uint64_t n, double rho, int *depth,
  * capacity).  Synchronises the device; clear != 0 resets them. */
 rs_status rs_device_errors(int clear, unsigned *flags);
 
+/* Test hook: select the leaf implementation (process-wide).
+ * RS_OPT_LEAF_PATH: 0 = automatic (default: warp-per-leaf kernels, bitmap
+ * kernels for leaf ranges <= 2^15, CTA kernel for leaves that do not fit);
+ * 1 = the CTA-per-leaf kernels for every leaf (so tests cover that path).
+ * Results are identical for every setting.  Unknown option -> RS_EINVAL. */
+enum { RS_OPT_LEAF_PATH = 1 };
+rs_status rs_set_option(int option, int value);
+
 /* Number of kernel launches issued by this thread since the last reset. */
 uint64_t rs_launch_count(int reset);
 

@@ -52,6 +52,7 @@ SIGNATURES = {
     "rs_plan": (_int, [_int, _u64, _u64, _dbl, C.POINTER(_int), C.POINTER(_int), _P64]),
     "rs_device_errors": (_int, [_int, C.POINTER(C.c_uint)]),
     "rs_launch_count": (_u64, [_int]),
+    "rs_set_option": (_int, [_int, _int]),
     "rs_timing_enable": (_int, [_int]),
     "rs_timing_read": (_int, [_int, C.POINTER(_dbl), _P64]),
     "rs_status_string": (C.c_char_p, [_int]),
@@ -269,6 +270,14 @@ def device_errors(clear: bool = True) -> int:
     f = C.c_uint()
     _check(lib().rs_device_errors(int(clear), C.byref(f)))
     return f.value
+
+
+OPT_LEAF_PATH = 1
+
+
+def set_option(option: int, value: int):
+    """Test hook (rs_set_option): OPT_LEAF_PATH 0 = automatic, 1 = CTA kernels only."""
+    _check(lib().rs_set_option(int(option), int(value)))
 
 
 def launch_count(reset: bool = False) -> int:

@@ -17,6 +17,7 @@ using namespace rs;
 namespace {
 
 thread_local rs_status t_last = RS_OK;
+int g_leaf_path = 0;                    // rs_set_option(RS_OPT_LEAF_PATH)
 thread_local uint64_t t_launches = 0;
 
 rs_status ret(rs_status s) { t_last = s; return s; }
@@ -224,7 +225,7 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
     const bool wr = (p.mode == RS_MODE_WR);
     void (*kern)(LeafArgs);
     size_t sm;
-    if (p.r_max <= BM_RMAX && p.mode == RS_MODE_WOR) {
+    if (p.r_max <= BM_RMAX && p.mode == RS_MODE_WOR && g_leaf_path == 0) {
         // small leaf ranges: warp per leaf over a bitmap (complement or WOR)
         la.out_base = p.shard_lo;
         void (*bk)(LeafArgs) = p.comp ? k_leaf_bitmap_comp : k_leaf_bitmap_wor;
@@ -238,7 +239,7 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         la.out_base = p.shard_lo;
         la.tiles_per_leaf = (p.r_max + COMP_TILE - 1) / COMP_TILE;
         kern = wide ? k_leaf_comp64 : k_leaf_comp32;
-    } else if (!wide) {
+    } else if (!wide && g_leaf_path == 0) {
         // common path: warp per leaf; leaves it cannot hold go to a spill
         // list that the CTA kernel completes right after (usually empty)
         u32 *spill_n = (u32 *)(ws + p.o_spill);
@@ -261,8 +262,10 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         ++t_launches;
         sp_leaf.end();
         return cuda_ok();
-    } else {
+    } else if (wide) {
         kern = wr ? k_leaf_wr64 : k_leaf_wor64;
+    } else {
+        kern = wr ? k_leaf_wr32 : k_leaf_wor32;
     }
     sm = wide ? sizeof(SLeaf<u64>) : sizeof(SLeaf<u32>);
     const u64 work = p.comp ? p.nleaves * la.tiles_per_leaf : p.nleaves;
@@ -587,6 +590,15 @@ rs_status rs_device_errors(int clear, unsigned *flags)
         if (cudaMemcpyToSymbol(g_rs_errors, &z, sizeof z) != cudaSuccess) return ret(RS_ECUDA);
     }
     return ret(RS_OK);
+}
+
+rs_status rs_set_option(int option, int value)
+{
+    if (option == RS_OPT_LEAF_PATH && (value == 0 || value == 1)) {
+        g_leaf_path = value;
+        return ret(RS_OK);
+    }
+    return ret(RS_EINVAL);
 }
 
 uint64_t rs_launch_count(int reset)

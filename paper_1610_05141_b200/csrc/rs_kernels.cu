@@ -112,7 +112,9 @@ __device__ __forceinline__ T skip_exact(double U, double lr, T r)
 
 // fp32 candidate for G (see above): sets ok when floor is certain; the
 // result saturates at r (any G >= r ends the chain).  Branch-free.
-__device__ __forceinline__ u32 skip_fast(u32 a, u32 b, float c, float m_abs, u32 r, bool &ok)
+// r is the chunk range saturated at 2^31 - 1; full says it is not saturated
+// (otherwise a G at or above the saturation point is not decided here).
+__device__ __forceinline__ u32 skip_fast(u32 a, u32 b, float c, float m_abs, u32 r, bool full, bool &ok)
 {
     const u64 m = ((((u64)a << 32) | b) >> 11) | 1ull;              // 2 * (u52 mantissa) + 1
     const float U = __ull2float_rn(m) * 0x1p-53f;                   // U rounded to fp32
@@ -120,7 +122,7 @@ __device__ __forceinline__ u32 skip_fast(u32 a, u32 b, float c, float m_abs, u32
     const float mg = m_abs + q * 0x1p-20f;
     const float lo = floorf(q - mg), hi = floorf(q + mg);
     const float rf = (float)r;
-    ok = lo >= rf || (lo == hi && lo >= 0.0f);
+    ok = (lo >= rf && full) || (lo == hi && lo >= 0.0f && lo < rf);
     return lo >= rf ? r : (u32)fminf(lo, rf);
 }
 
@@ -170,6 +172,7 @@ __device__ __forceinline__ void bernoulli_chunks(const BernArgs &a)
             const u64 lo = bound_at(a.N, a.Db, gi);
             const T r = (T)(bound_at(a.N, a.Db, gi + 1) - lo);
             const u32 r32 = r > (T)0x7fffffffu ? 0x7fffffffu : (u32)r;    // fast path saturation point
+            const bool rfull = r <= (T)0x7fffffffu;
             const Stream st(a.seed, P_GEO, ((u64)1 << a.Db) + gi);
             B *bg = bw + total;
             const u32 room = CAP - total;
@@ -179,8 +182,8 @@ __device__ __forceinline__ void bernoulli_chunks(const BernArgs &a)
             for (u32 q0 = 0;; q0 += 32) {
                 const u32x4 w = philox_rk(q0 + lane, st, a.rk);
                 bool ok0, ok1;
-                const u32 g0 = skip_fast(w.x, w.y, c, m_abs, r32, ok0);
-                const u32 g1 = skip_fast(w.z, w.w, c, m_abs, r32, ok1);
+                const u32 g0 = skip_fast(w.x, w.y, c, m_abs, r32, rfull, ok0);
+                const u32 g1 = skip_fast(w.z, w.w, c, m_abs, r32, rfull, ok1);
                 T s0 = (T)g0 + 1, s1 = (T)g1 + 1;
                 if (__any_sync(0xffffffffu, !(ok0 && ok1))) {  // rare: exact fp64 (CANON)
                     if (!ok0) s0 = skip_exact<T>(u52(w.x, w.y), a.log1m_rho, r);

@@ -101,3 +101,12 @@ def test_no_cpu_fallback():
     # the raw C call reports RS_ECUDA rather than computing anything
     st = rs.lib().rs_sample_wor(100, 10, 1, ctypes.c_void_p(0), ctypes.c_void_p(0))
     assert st == 2
+
+
+def test_set_option_host_only():
+    rs.set_option(rs.OPT_LEAF_PATH, 1)
+    rs.set_option(rs.OPT_LEAF_PATH, 0)
+    with pytest.raises(rs.RSError):
+        rs.set_option(99, 0)
+    with pytest.raises(rs.RSError):
+        rs.set_option(rs.OPT_LEAF_PATH, 7)

@@ -67,6 +67,24 @@ def test_wor_full_compare(N, n):
     _no_device_errors()
 
 
+# the CTA-per-leaf kernels (the spill path of the warp kernels) on every leaf
+CTA_CASES = [(2 ** 30, 2 ** 20), (12345, 6172), (2 ** 22, 3 * 2 ** 20), (2 ** 24, 2 ** 24 - 3),
+             (10 ** 9 + 7, 100003), (2 ** 21, 2 ** 20)]
+
+
+@pytest.mark.parametrize("N,n", CTA_CASES)
+def test_wor_cta_path(N, n):
+    rs.set_option(rs.OPT_LEAF_PATH, 1)
+    try:
+        got = _np(rs.sample_wor(N, n, 7))
+        gwr = _np(rs.sample_wr(N, n, 7))
+    finally:
+        rs.set_option(rs.OPT_LEAF_PATH, 0)
+    assert np.array_equal(got, O.sample_wor(N, n, 7))
+    assert np.array_equal(gwr, O.sample_wr(N, n, 7))
+    _no_device_errors()
+
+
 # ---- with replacement --------------------------------------------------------
 
 WR_CASES = [(1, 5), (4, 1000), (2, 3), (100, 100), (2 ** 24, 2 ** 20), (10 ** 9 + 7, 100003),
@@ -84,8 +102,10 @@ def test_wr_full_compare(N, n):
 
 # ---- Bernoulli -------------------------------------------------------------------
 
+# chunk ranges r <= 2^16 (u16 buffers, 4 chunks per ticket), <= 2^24 (u32), above (u64)
 BERN_CASES = [(2 ** 24, 0.01), (10 ** 6 + 17, 0.3), (2 ** 20, 1e-3), (1000, 0.999), (5, 0.5),
-              (2 ** 26, 1e-5), (1000, 0.0), (1000, 1.0), (0, 0.5)]
+              (2 ** 26, 1e-5), (1000, 0.0), (1000, 1.0), (0, 0.5), (2 ** 30, 1e-6),
+              (2 ** 40 + 3, 1e-9), (3 * 10 ** 8, 0.5)]
 
 
 @pytest.mark.parametrize("N,rho", BERN_CASES)
