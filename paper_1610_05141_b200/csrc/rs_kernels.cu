@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split(SplitArgs a)
     }
 }
 
-__global__ void __launch_bounds__(LEVEL_NT, 8) k_split_level(LevelArgs a)
+__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_level(LevelArgs a)
 {
     const u64 j = (u64)blockIdx.x * LEVEL_NT + threadIdx.x;
     if (j >= a.width) return;

@@ -98,7 +98,7 @@ struct LevelArgs {
     u32 *leaf_cnt;                 // leaf level: u32 counts + u64 offsets
     u64 *leaf_off;
 };
-__global__ void __launch_bounds__(LEVEL_NT, 8) k_split_level(LevelArgs a);
+__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_level(LevelArgs a);
 
 // ---------------------------------------------------------------------------
 // Leaf kernels (rows a5/a6/a7/a8).
