@@ -382,14 +382,16 @@ rs_status bern_call(u64 N, double rho, u64 seed, int world, int rank, u64 *out, 
     Span sp(2, cs);
     {
         const u64 rmax = (N >> p.Db) + 1;
-        void (*bk)(BernArgs) = rmax <= (1ull << 16) ? k_bernoulli : rmax <= (1ull << 24) ? k_bernoulli32 : k_bernoulli64;
+        const bool r16 = rmax <= (1ull << 16);
+        void (*bk)(BernArgs) = r16 ? k_bernoulli : rmax <= (1ull << 24) ? k_bernoulli32 : k_bernoulli64;
+        const int nt = r16 ? 32 * BNW16 : 32 * BW_WARPS;
         int per = 0, dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(bk, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk, 128, 0) != cudaSuccess || per < 1) per = 1;
-        const u64 need = (p.nchunks + 3) / 4, g = (u64)sms * per;   // (over-provisioned: tickets end the loop)
-        bk<<<(unsigned)(need < g ? need : g), 128, 0, cs>>>(a);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk, nt, 0) != cudaSuccess || per < 1) per = 1;
+        const u64 need = (p.nchunks + nt / 32 - 1) / (nt / 32), g = (u64)sms * per;
+        bk<<<(unsigned)(need < g ? need : g), nt, 0, cs>>>(a);
     }
     sp.end();
     ++t_launches;

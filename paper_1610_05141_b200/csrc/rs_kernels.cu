@@ -145,10 +145,10 @@ constexpr int BW_WARPS = 4;
 // positions (type B, relative to each chunk start) in shared memory, looks
 // back over tickets, then stores.  T = position arithmetic (u32 while a
 // batch's 64 steps fit, else u64).
-template <typename T, typename B, int G, u32 CAP>
+template <typename T, typename B, int G, u32 CAP, int NW>
 __device__ __forceinline__ void bernoulli_chunks(const BernArgs &a)
 {
-    __shared__ B buf[BW_WARPS][CAP];
+    __shared__ B buf[NW][CAP];
     const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     B *bw = buf[wid];
     const float c = (float)(0x1.62e42fefa39efp-1 / a.log1m_rho);   // ln 2 / lr
@@ -242,6 +242,10 @@ __device__ __forceinline__ void bernoulli_chunks(const BernArgs &a)
                 dinc = __reduce_min_sync(0xffffffffu, dinc);
                 dpen = __reduce_min_sync(0xffffffffu, dpen);
                 if (dpen < dinc) {                          // a nearer predecessor is not published yet
+#ifndef RS_BSLEEP
+#define RS_BSLEEP 2000
+#endif
+                    __nanosleep(RS_BSLEEP);                 // yield issue slots to generating warps
 #pragma unroll
                     for (int t = 0; t < 4; ++t) {
                         const long long idx = p - (long long)(4 * lane + t);
@@ -285,11 +289,17 @@ __device__ __forceinline__ void bernoulli_chunks(const BernArgs &a)
 }
 
 // chunk range r <= 2^16: u16 positions, 4 chunks per ticket (4864 x 2 B per warp)
-__global__ void __launch_bounds__(32 * BW_WARPS) k_bernoulli(BernArgs a) { bernoulli_chunks<u32, uint16_t, 4, 4864>(a); }
+#ifndef RS_BG
+#define RS_BG 4
+#endif
+constexpr int BG16 = RS_BG;                                           // chunks per ticket (u16 path)
+constexpr u32 BCAP16 = ((BG16 * 1024 + 10 * 32 * (BG16 < 4 ? 2 : BG16 / 2) + 63) / 64) * 64;
+constexpr int BNW16 = (BCAP16 * 2 * 4 <= 48 * 1024) ? 4 : (BCAP16 * 2 * 2 <= 48 * 1024) ? 2 : 1;
+__global__ void __launch_bounds__(32 * BNW16) k_bernoulli(BernArgs a) { bernoulli_chunks<u32, uint16_t, BG16, BCAP16, BNW16>(a); }
 // r <= 2^24: u32 positions, 2 chunks per ticket (2560 x 4 B per warp)
-__global__ void __launch_bounds__(32 * BW_WARPS) k_bernoulli32(BernArgs a) { bernoulli_chunks<u32, u32, 2, 2560>(a); }
+__global__ void __launch_bounds__(32 * BW_WARPS) k_bernoulli32(BernArgs a) { bernoulli_chunks<u32, u32, 2, 2560, BW_WARPS>(a); }
 // larger r: u64 positions, 1 chunk per ticket (1536 x 8 B per warp)
-__global__ void __launch_bounds__(32 * BW_WARPS) k_bernoulli64(BernArgs a) { bernoulli_chunks<u64, u64, 1, 1536>(a); }
+__global__ void __launch_bounds__(32 * BW_WARPS) k_bernoulli64(BernArgs a) { bernoulli_chunks<u64, u64, 1, 1536, BW_WARPS>(a); }
 
 // ===========================================================================
 // Validation helpers.

@@ -159,7 +159,7 @@ struct BernArgs {
     RoundKeys rk;          // Philox round keys of seed
 };
 
-__global__ void __launch_bounds__(128) k_bernoulli(BernArgs a);     // chunk ranges <= 2^16
+__global__ void k_bernoulli(BernArgs a);                           // chunk ranges <= 2^16
 __global__ void __launch_bounds__(128) k_bernoulli32(BernArgs a);   // chunk ranges <= 2^24
 __global__ void __launch_bounds__(128) k_bernoulli64(BernArgs a);   // larger chunk ranges
 

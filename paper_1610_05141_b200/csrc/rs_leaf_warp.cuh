@@ -146,8 +146,10 @@ __device__ __forceinline__ u32 wl_count(WarpLeaf &sh, const RoundKeys &K, const 
         if (q2 < qfull) {
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
+#ifndef RS_EXP_NOCOUNT
                 atomicAdd(&sh.cnt[wl_word(v[w] >> shb)], 1u);
                 atomicAdd(&sh.cnt[wl_word(v2[w] >> shb)], 1u);
+#endif
             }
         } else {
 #pragma unroll
@@ -264,7 +266,11 @@ __device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const RoundKeys &K, con
         if (full) {
 #pragma unroll
             for (int e = 4 * m0; e < 4 * (m0 + GB); ++e)
+#ifdef RS_EXP_NOSCATTER
+                pos[e - 4 * m0] = 4 * (lane + 32u * (e >> 2)) + (e & 3);
+#else
                 pos[e - 4 * m0] = atomicAdd(&sh.cnt[wl_word(x[e] >> shb)], 1u);
+#endif
 #pragma unroll
             for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) kh[pos[e - 4 * m0]] = x[e];
         } else if (4 * (lane + 32u * m0) < J) {
