@@ -381,7 +381,7 @@ rs_status bern_call(u64 N, double rho, u64 seed, int world, int rank, u64 *out, 
     a.rk = round_keys(seed);
     Span sp(2, cs);
     {
-        const u64 rmax = (N >> p.Db) + 1;
+        const u64 rmax = (N >> p.Db) + ((N & ((1ull << p.Db) - 1)) != 0);   // largest chunk range
         const bool r16 = rmax <= (1ull << 16);
         void (*bk)(BernArgs) = r16 ? k_bernoulli : rmax <= (1ull << 24) ? k_bernoulli32 : k_bernoulli64;
         const int nt = r16 ? 32 * BNW16 : 32 * BW_WARPS;
