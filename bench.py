@@ -333,7 +333,8 @@ def run_native(args):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(wl["name"])
+            t = json.load(f).get(wl["name"])
+            traffic = float(t["bytes_per_launch"]) if t else None
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -80,13 +80,30 @@ __device__ __forceinline__ void bitmap_leaves(const LeafArgs &a)
         // emit the output bits in order; dense: one word per step, lane = bit,
         // so consecutive lanes store consecutive outputs
         if (nout * 4 >= (u64)r) {
+            // four words per step (16-byte broadcast load): independent
+            // prefix chains and stores; the last partial word is masked
+            const u32 lm = (1u << lane) - 1u;
+            const u32 nfull = r >> 5;               // words with all 32 values in range
             u32 pos = 0;
+            u64 vb = base + lane;
+            u32 w = 0;
 #pragma unroll 1
-            for (u32 w = 0; w < nw; ++w) {
+            for (; w + 4 <= nfull; w += 4, vb += 128) {
+                const uint4 W4 = *reinterpret_cast<const uint4 *>(&sh.bm[w]);
+                const u32 b0 = COMP ? ~W4.x : W4.x, b1 = COMP ? ~W4.y : W4.y;
+                const u32 b2 = COMP ? ~W4.z : W4.z, b3 = COMP ? ~W4.w : W4.w;
+                const u32 p0 = pos, p1 = p0 + __popc(b0), p2 = p1 + __popc(b1), p3 = p2 + __popc(b2);
+                pos = p3 + __popc(b3);
+                if ((b0 >> lane) & 1u) dst[p0 + __popc(b0 & lm)] = vb;
+                if ((b1 >> lane) & 1u) dst[p1 + __popc(b1 & lm)] = vb + 32;
+                if ((b2 >> lane) & 1u) dst[p2 + __popc(b2 & lm)] = vb + 64;
+                if ((b3 >> lane) & 1u) dst[p3 + __popc(b3 & lm)] = vb + 96;
+            }
+#pragma unroll 1
+            for (; w < nw; ++w, vb += 32) {
                 const u32 word = sh.bm[w];
                 const u32 bits = COMP ? (~word & bm_valid(w, r)) : word;
-                if ((bits >> lane) & 1u)
-                    dst[pos + __popc(bits & ((1u << lane) - 1u))] = base + 32u * w + lane;
+                if ((bits >> lane) & 1u) dst[pos + __popc(bits & lm)] = vb;
                 pos += __popc(bits);
             }
         } else {
