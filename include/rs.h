@@ -92,6 +92,23 @@ rs_status rs_bernoulli_shard(uint64_t N, double rho, uint64_t seed, int world, i
                              uint64_t *out_local, uint64_t capacity, uint64_t *count_dev,
                              void *stream);
 
+/* ---- any node of the split tree: range-addressable sampling (NEXT-1) -----
+ * The online / "sorted output in batches" use of Algorithm R:
+ * node (depth, index), 0 <= depth <= D (the tree depth, rs_plan), index <
+ * 2^depth, covers the dyadic value range [floor(index N / 2^depth),
+ * floor((index+1) N / 2^depth)) (+1 for the 1-based values).
+ * rs_node_info: the node's output count and its offset in the full output,
+ * by host path replay of the depth splits above it (no device; same
+ * arithmetic as the kernels).  rs_sample_node: the node's slice of
+ * rs_sample_wor (mode RS_MODE_WOR, complement rule included) or rs_sample_wr
+ * (RS_MODE_WR) into out[0..count) (device).  The slices of the nodes of any
+ * partition of the leaf range, in order, concatenate to the full output.
+ * depth > D or index out of range -> RS_EINVAL. */
+rs_status rs_node_info(int mode, uint64_t N, uint64_t n, uint64_t seed, int depth, uint64_t index,
+                       uint64_t *count, uint64_t *global_offset);
+rs_status rs_sample_node(int mode, uint64_t N, uint64_t n, uint64_t seed, int depth,
+                         uint64_t index, uint64_t *out, void *stream);
+
 /* ---- caller-provided workspace variants --------------------------------
  * rs_workspace_bytes: bytes of device workspace the *_ws calls need for
  * (mode, N, n or rho, world).  ws must be 256-byte aligned.  Too small ->
@@ -115,8 +132,11 @@ rs_status rs_sample_wor_host(uint64_t N, uint64_t n, uint64_t seed, uint64_t *ou
 
 /* Host-buffer call for any mode/shard: the rank's slice of rs_sample_wor
  * (mode RS_MODE_WOR) or rs_sample_wr (RS_MODE_WR) into out_host[0..count),
- * count = rs_shard_info's local_count.  Synchronous (returns after the
- * device->host copy completed on `stream`). */
+ * count = rs_shard_info's local_count.  Generates the slice node by node
+ * (rs_sample_node; batches of <= 2^27 values) into two device staging
+ * buffers, copying batch i to the host on an internal stream while batch
+ * i+1 is generated on `stream`.  Synchronous (returns after the last copy).
+ * out_host should be pinned for full copy bandwidth. */
 rs_status rs_sample_shard_host(int mode, uint64_t N, uint64_t n, uint64_t seed, int world,
                                int rank, uint64_t *out_host, void *stream);
 

@@ -53,6 +53,8 @@ SIGNATURES = {
     "rs_device_errors": (_int, [_int, C.POINTER(C.c_uint)]),
     "rs_launch_count": (_u64, [_int]),
     "rs_set_option": (_int, [_int, _int]),
+    "rs_node_info": (_int, [_int, _u64, _u64, _u64, _int, _u64, _P64, _P64]),
+    "rs_sample_node": (_int, [_int, _u64, _u64, _u64, _int, _u64, _vp, _vp]),
     "rs_timing_enable": (_int, [_int]),
     "rs_timing_read": (_int, [_int, C.POINTER(_dbl), _P64]),
     "rs_status_string": (C.c_char_p, [_int]),
@@ -273,6 +275,51 @@ def device_errors(clear: bool = True) -> int:
 
 
 OPT_LEAF_PATH = 1
+
+
+def node_info(mode: int, N: int, n: int, seed: int, depth: int, index: int):
+    """(count, global_offset) of split-tree node (depth, index) (host replay)."""
+    c, off = C.c_uint64(), C.c_uint64()
+    _check(lib().rs_node_info(int(mode), N, n, seed % 2**64, int(depth), int(index), C.byref(c),
+                              C.byref(off)))
+    return c.value, off.value
+
+
+def sample_node(mode: int, N: int, n: int, seed: int, depth: int, index: int, out=None,
+                device="cuda", stream=None):
+    """The node's slice of the full WOR / WR output (device tensor)."""
+    _require_cuda()
+    cnt, _ = node_info(mode, N, n, seed, depth, index)
+    o = _out(cnt, out, device)
+    _check(lib().rs_sample_node(int(mode), N, n, seed % 2**64, int(depth), int(index), _ptr(o),
+                                _stream(stream)))
+    return o[:cnt]
+
+
+def leaf_range_nodes(D: int, lo: int, hi: int):
+    """Canonical decomposition of the leaf range [lo, hi) at depth D into
+    maximal aligned dyadic nodes (depth, index), left to right."""
+    out = []
+    while lo < hi:
+        size = lo & -lo if lo else 1 << D
+        while size > hi - lo:
+            size >>= 1
+        d = D - (size.bit_length() - 1)
+        out.append((d, lo >> (D - d)))
+        lo += size
+    return out
+
+
+def sample_range(mode: int, N: int, n: int, seed: int, leaf_lo: int, leaf_hi: int, stream=None):
+    """Leaves [leaf_lo, leaf_hi) of the full output -- any contiguous slice of
+    the sorted sample, e.g. for larger-than-HBM samples in batches (NEXT-1).
+    Returns (device tensor, global offset of its first value)."""
+    D = plan(mode, N, n)[0]
+    nodes = leaf_range_nodes(D, leaf_lo, leaf_hi)
+    if not nodes:
+        return torch.empty(0, dtype=torch.uint64, device="cuda"), 0
+    parts = [sample_node(mode, N, n, seed, d, i, stream=stream) for d, i in nodes]
+    return torch.cat(parts), node_info(mode, N, n, seed, *nodes[0])[1]
 
 
 def set_option(option: int, value: int):

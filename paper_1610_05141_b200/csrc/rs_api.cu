@@ -93,9 +93,10 @@ int log2_world(int world)
 struct TreePlan {
     int mode;               // RS_MODE_WOR / RS_MODE_WR
     u64 N, n, m, seed;
-    int D, s, rank;
+    int D, s;
+    u64 idx;                // the subtree root is node (s, idx)
     bool comp;
-    u64 root_cnt;           // core count of the shard's subtree root (s, rank)
+    u64 root_cnt;           // core count of the subtree root (s, idx)
     u64 root_core_off;      // core offset of that root in the world=1 tree
     u64 shard_lo, shard_hi; // shard's offsets [lo, hi)
     u64 leaf0, nleaves;     // shard's leaves
@@ -106,34 +107,38 @@ struct TreePlan {
     size_t o_ping_cnt, o_ping_off, o_pong_cnt, o_pong_off, o_leaf_cnt, o_leaf_off, o_spill, bytes;
 };
 
-rs_status plan_tree(int mode, u64 N, u64 n, u64 seed, int world, int rank, TreePlan &p)
+// Plan for the subtree rooted at node (s, idx) of the split tree, s <= D:
+// Algorithm P's path replay gives its count and its offset in the global
+// output ("<= ceil(log p) hypergeometric random deviates").  Shards
+// are the nodes at depth log2(world); ranges of leaves are unions of nodes.
+rs_status plan_node(int mode, u64 N, u64 n, u64 seed, int s, u64 idx, TreePlan &p)
 {
     memset(&p, 0, sizeof p);
     if (N >= (1ull << 63)) return RS_EINVAL;
     if (mode == RS_MODE_WOR && n > N) return RS_EINVAL;
     if (mode == RS_MODE_WR && N == 0 && n > 0) return RS_EINVAL;
     if (n >= (1ull << 40)) return RS_EINVAL;            // > 8 TiB of output
-    const int s = log2_world(world);
-    if (s < 0 || rank < 0 || rank >= world) return RS_EINVAL;
-    p.mode = mode; p.N = N; p.n = n; p.seed = seed; p.s = s; p.rank = rank;
+    p.mode = mode; p.N = N; p.n = n; p.seed = seed;
     p.comp = (mode == RS_MODE_WOR) && (n > N - n);      // R8: 2n > N
     p.m = p.comp ? N - n : n;
     p.D = tree_depth(p.m);
+    if (s < 0 || s > p.D || s > 62 || idx >= (1ull << s)) return RS_EINVAL;
+    p.s = s; p.idx = idx;
     // Algorithm P (Fig. 2): follow the s splits on the root path
     u64 k = p.m, off = 0;
     for (int e = 0; e < s; ++e) {
-        const u64 anc = (u64)rank >> (s - e);
+        const u64 anc = idx >> (s - e);
         const u64 x = split_node(mode == RS_MODE_WR, N, e, anc, k, seed);
-        if (((u64)rank >> (s - e - 1)) & 1) { off += x; k -= x; } else { k = x; }
+        if ((idx >> (s - e - 1)) & 1) { off += x; k -= x; } else { k = x; }
     }
     p.root_cnt = k;
     p.root_core_off = off;
-    p.shard_lo = bound_at(N, s, (u64)rank);
-    p.shard_hi = bound_at(N, s, (u64)rank + 1);
+    p.shard_lo = bound_at(N, s, idx);
+    p.shard_hi = bound_at(N, s, idx + 1);
     p.local_count = p.comp ? (p.shard_hi - p.shard_lo) - k : k;
     p.global_offset = p.comp ? p.shard_lo - off : off;
     p.nleaves = 1ull << (p.D - s);
-    p.leaf0 = (u64)rank << (p.D - s);
+    p.leaf0 = idx << (p.D - s);
     p.r_max = (N >> p.D) + ((N & ((1ull << p.D) - 1)) != 0);
     // split: one CTA expands depths s..s+top, then one launch per level
     p.top = (p.D - s) < SPLIT_TOP ? (p.D - s) : SPLIT_TOP;
@@ -148,6 +153,14 @@ rs_status plan_tree(int mode, u64 N, u64 n, u64 seed, int world, int rank, TreeP
     p.o_spill = o; o = align256(o + (p.nleaves + 1) * 4);   // spill count + list
     p.bytes = o;
     return RS_OK;
+}
+
+// Shard rank of world = 2^s (s <= 3): node (s, rank).
+rs_status plan_tree(int mode, u64 N, u64 n, u64 seed, int world, int rank, TreePlan &p)
+{
+    const int s = log2_world(world);
+    if (s < 0 || rank < 0 || rank >= world) { memset(&p, 0, sizeof p); return RS_EINVAL; }
+    return plan_node(mode, N, n, seed, s, (u64)rank, p);
 }
 
 template <typename F>
@@ -189,7 +202,7 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         SplitArgs a;
         memset(&a, 0, sizeof a);
         a.N = p.N; a.seed = p.seed; a.wr = (p.mode == RS_MODE_WR);
-        a.ds = p.s; a.nlev = p.top; a.node0 = (u64)p.rank;
+        a.ds = p.s; a.nlev = p.top; a.node0 = p.idx;
         a.root_cnt = p.root_cnt; a.root_off = 0;        // offsets local to the shard
         if (p.s + p.top == p.D) { a.leaf_cnt = leaf_cnt; a.leaf_off = leaf_off; }
         else { a.out_cnt = ping_cnt; a.out_off = ping_off; }
@@ -202,7 +215,7 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         memset(&a, 0, sizeof a);
         a.N = p.N; a.seed = p.seed; a.wr = (p.mode == RS_MODE_WR); a.d = d;
         a.width = 1ull << (d - p.s);
-        a.node0 = (u64)p.rank << (d - p.s);
+        a.node0 = p.idx << (d - p.s);
         a.in_cnt = in_cnt; a.in_off = in_off;
         const bool flip = ((d - p.s - p.top) & 1) == 0;
         u64 *oc = flip ? pong_cnt : ping_cnt, *oo = flip ? pong_off : ping_off;
@@ -276,13 +289,9 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
     return cuda_ok();
 }
 
-rs_status tree_call(int mode, u64 N, u64 n, u64 seed, int world, int rank, u64 *out,
-                    void *ws, size_t ws_bytes, void *stream)
+rs_status plan_call(const TreePlan &p, u64 *out, void *ws, size_t ws_bytes, void *stream)
 {
     if (!have_device()) return RS_ECUDA;
-    TreePlan p;
-    rs_status st = plan_tree(mode, N, n, seed, world, rank, p);
-    if (st != RS_OK) return st;
     if (p.local_count == 0) return RS_OK;
     if (!out) return RS_EINVAL;
     const cudaStream_t cs = S(stream);
@@ -294,9 +303,19 @@ rs_status tree_call(int mode, u64 N, u64 n, u64 seed, int world, int rank, u64 *
     } else if (ws_bytes < p.bytes) {
         return RS_ENOMEM;
     }
-    st = run_tree(p, out, w, cs);
+    const rs_status st = run_tree(p, out, w, cs);
     if (own) cudaFreeAsync(w, cs);
     return st;
+}
+
+rs_status tree_call(int mode, u64 N, u64 n, u64 seed, int world, int rank, u64 *out,
+                    void *ws, size_t ws_bytes, void *stream)
+{
+    if (!have_device()) return RS_ECUDA;
+    TreePlan p;
+    const rs_status st = plan_tree(mode, N, n, seed, world, rank, p);
+    if (st != RS_OK) return st;
+    return plan_call(p, out, ws, ws_bytes, stream);
 }
 
 // ---------------------------------------------------------------------------
@@ -507,25 +526,88 @@ rs_status rs_bernoulli_ws(uint64_t N, double rho, uint64_t seed, int world, int 
                          stream));
 }
 
+rs_status rs_node_info(int mode, uint64_t N, uint64_t n, uint64_t seed, int depth, uint64_t index,
+                       uint64_t *count, uint64_t *global_offset)
+{
+    if (mode != RS_MODE_WOR && mode != RS_MODE_WR) return ret(RS_EINVAL);
+    TreePlan p;
+    const rs_status st = plan_node(mode, N, n, seed, depth, index, p);
+    if (st != RS_OK) return ret(st);
+    if (count) *count = p.local_count;
+    if (global_offset) *global_offset = p.global_offset;
+    return ret(RS_OK);
+}
+
+rs_status rs_sample_node(int mode, uint64_t N, uint64_t n, uint64_t seed, int depth,
+                         uint64_t index, uint64_t *out, void *stream)
+{
+    if (mode != RS_MODE_WOR && mode != RS_MODE_WR) return ret(RS_EINVAL);
+    TreePlan p;
+    const rs_status st = plan_node(mode, N, n, seed, depth, index, p);
+    if (st != RS_OK) return ret(st);
+    return ret(plan_call(p, out, nullptr, 0, stream));
+}
+
 rs_status rs_sample_shard_host(int mode, uint64_t N, uint64_t n, uint64_t seed, int world,
                                int rank, uint64_t *out_host, void *stream)
 {
     if (!have_device()) return ret(RS_ECUDA);
     if (mode != RS_MODE_WOR && mode != RS_MODE_WR) return ret(RS_EINVAL);
-    TreePlan p;
-    rs_status st = plan_tree(mode, N, n, seed, world, rank, p);
+    TreePlan sp;
+    rs_status st = plan_tree(mode, N, n, seed, world, rank, sp);
     if (st != RS_OK) return ret(st);
-    if (p.local_count == 0) return ret(RS_OK);
+    if (sp.local_count == 0) return ret(RS_OK);
     if (!out_host) return ret(RS_EINVAL);
-    const cudaStream_t cs = S(stream);
-    u64 *dev = nullptr;
-    if (cudaMallocAsync((void **)&dev, p.local_count * 8, cs) != cudaSuccess) return ret(RS_ENOMEM);
-    st = tree_call(mode, N, n, seed, world, rank, dev, nullptr, 0, stream);
-    if (st == RS_OK &&
-        cudaMemcpyAsync(out_host, dev, p.local_count * 8, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
-        st = RS_ECUDA;
-    cudaFreeAsync(dev, cs);
-    if (cudaStreamSynchronize(cs) != cudaSuccess) st = RS_ECUDA;
+    // batches: the shard's descendants at depth s + b, each <= 2^27 values
+    int b = 0;
+    while (b < sp.D - sp.s && (sp.local_count >> b) > (1ull << 27)) ++b;
+    if (b < sp.D - sp.s && b < 20 && sp.local_count > (1ull << 26)) ++b;   // >= 2 batches to overlap
+    const u64 nb = 1ull << b;
+    std::vector<TreePlan> plans(nb);
+    u64 maxc = 0;
+    size_t maxws = 0;
+    for (u64 i = 0; i < nb; ++i) {
+        st = plan_node(mode, N, n, seed, sp.s + b, (sp.idx << b) + i, plans[i]);
+        if (st != RS_OK) return ret(st);
+        if (plans[i].local_count > maxc) maxc = plans[i].local_count;
+        if (plans[i].bytes > maxws) maxws = plans[i].bytes;
+    }
+    const cudaStream_t gs = S(stream);
+    cudaStream_t cs;
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return ret(RS_ECUDA);
+    cudaEvent_t gen_done[2], copy_done[2];
+    for (int i = 0; i < 2; ++i) {
+        cudaEventCreateWithFlags(&gen_done[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&copy_done[i], cudaEventDisableTiming);
+    }
+    u64 *buf[2] = {nullptr, nullptr};
+    unsigned char *ws = nullptr;
+    st = RS_OK;
+    if (cudaMallocAsync((void **)&buf[0], maxc * 8 + 8, gs) != cudaSuccess ||
+        cudaMallocAsync((void **)&buf[1], maxc * 8 + 8, gs) != cudaSuccess ||
+        cudaMallocAsync((void **)&ws, maxws, gs) != cudaSuccess)
+        st = RS_ENOMEM;
+    const u64 base_off = sp.global_offset;
+    for (u64 i = 0; i < nb && st == RS_OK; ++i) {
+        const int j = (int)(i & 1);
+        if (i >= 2) cudaStreamWaitEvent(gs, copy_done[j], 0);       // buffer j is free again
+        st = run_tree(plans[i], buf[j], ws, gs);
+        cudaEventRecord(gen_done[j], gs);
+        cudaStreamWaitEvent(cs, gen_done[j], 0);
+        if (plans[i].local_count &&
+            cudaMemcpyAsync(out_host + (plans[i].global_offset - base_off), buf[j],
+                            plans[i].local_count * 8, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+            st = RS_ECUDA;
+        cudaEventRecord(copy_done[j], cs);
+    }
+    cudaStreamWaitEvent(gs, copy_done[0], 0);
+    cudaStreamWaitEvent(gs, copy_done[1], 0);
+    if (buf[0]) cudaFreeAsync(buf[0], gs);
+    if (buf[1]) cudaFreeAsync(buf[1], gs);
+    if (ws) cudaFreeAsync(ws, gs);
+    if (cudaStreamSynchronize(gs) != cudaSuccess || cudaStreamSynchronize(cs) != cudaSuccess) st = RS_ECUDA;
+    for (int i = 0; i < 2; ++i) { cudaEventDestroy(gen_done[i]); cudaEventDestroy(copy_done[i]); }
+    cudaStreamDestroy(cs);
     return ret(st);
 }
 

@@ -110,3 +110,37 @@ def test_set_option_host_only():
         rs.set_option(99, 0)
     with pytest.raises(rs.RSError):
         rs.set_option(rs.OPT_LEAF_PATH, 7)
+
+
+def test_leaf_range_nodes_partition():
+    for D in (3, 5, 8):
+        for lo in range(0, 1 << D, 3):
+            for hi in range(lo, (1 << D) + 1, 5):
+                nodes = rs.leaf_range_nodes(D, lo, hi)
+                cur = lo
+                for d, i in nodes:
+                    assert 0 <= d <= D and 0 <= i < (1 << d)
+                    assert i << (D - d) == cur          # aligned and contiguous
+                    cur += 1 << (D - d)
+                assert cur == hi
+
+
+@pytest.mark.parametrize("N,n,mode", [(2 ** 30, 2 ** 20, 0), (2 ** 48, 2 ** 32, 0), (2 ** 36, 2 ** 32, 1),
+                                      (2 ** 32, 3 * 2 ** 30, 0), (10 ** 9 + 7, 100003, 0)])
+def test_node_info_matches_oracle_replay(N, n, mode):
+    """rs_node_info (librs host replay) vs the oracle's independent replay
+    (rso_path) for nodes at every depth down to the leaves."""
+    D, comp, m = O.plan(N, n, mode)
+    wr = mode == 1
+    for d in sorted(set([0, 1, 3, min(D, 7), D])):
+        for i in sorted(set([0, (1 << d) - 1, (1 << d) // 3])):
+            cnt, off = rs.node_info(mode, N, n, 1, d, i)
+            c, o = O.path(N, m, 1, d, i, wr)
+            if comp:
+                lo, R, _ = O.node(N, d, i)
+                c, o = R - c, lo - o
+            assert (cnt, off) == (c, o), (d, i)
+    with pytest.raises(rs.RSError):
+        rs.node_info(mode, N, n, 1, D + 1, 0)
+    with pytest.raises(rs.RSError):
+        rs.node_info(mode, N, n, 1, 2, 4)

@@ -237,3 +237,30 @@ def test_workspace_variant():
     assert np.array_equal(_np(out), O.sample_wor(N, n, 1))
     with pytest.raises(rs.RSError):
         rs.sample_wor_ws(N, n, 1, 1, 0, out, ws[: wsb // 2])
+
+
+# ---- NEXT-1: any node / leaf range of the tree (range-addressable sampling) ------
+
+@pytest.mark.parametrize("N,n,mode", [(2 ** 30, 2 ** 20, 0), (2 ** 22, 3 * 2 ** 20, 0),
+                                      (2 ** 24, 2 ** 20, 1), (10 ** 9 + 7, 100003, 0)])
+def test_nodes_and_ranges(N, n, mode):
+    full = _np(rs.sample_wr(N, n, 11) if mode else rs.sample_wor(N, n, 11))
+    D = rs.plan(mode, N, n)[0]
+    for d in sorted(set([0, 2, 5, D])):
+        for i in sorted(set(i for i in [0, 1, (1 << d) // 2, (1 << d) - 1] if i < (1 << d))):
+            cnt, off = rs.node_info(mode, N, n, 11, d, i)
+            got = _np(rs.sample_node(mode, N, n, 11, d, i))
+            assert got.size == cnt
+            assert np.array_equal(got, full[off: off + cnt]), (d, i)
+    for lo, hi in [(0, 1 << D), (3, 17), ((1 << D) // 3, (1 << D) - 5), (7, 8)]:
+        got, off = rs.sample_range(mode, N, n, 11, lo, hi)
+        assert np.array_equal(_np(got), full[off: off + got.numel()]), (lo, hi)
+
+
+def test_host_buffer_batched_overlap():
+    # > 2^26 values: the host path runs several node batches, copies overlapped
+    N, n = 2 ** 40, 3 * 2 ** 26 + 12345
+    h = rs.sample_wor_host(N, n, 5)
+    d = rs.sample_wor(N, n, 5)
+    assert torch.equal(h.view(torch.int64), d.cpu().view(torch.int64))
+    _sampled_leaf_parity(d, N, n, 5, O.MODE_WOR, nsample=16)
