@@ -403,13 +403,13 @@ rs_status bern_call(u64 N, double rho, u64 seed, int world, int rank, u64 *out, 
         const u64 rmax = (N >> p.Db) + ((N & ((1ull << p.Db) - 1)) != 0);   // largest chunk range
         const bool r16 = rmax <= (1ull << 16);
         void (*bk)(BernArgs) = r16 ? k_bernoulli : rmax <= (1ull << 24) ? k_bernoulli32 : k_bernoulli64;
-        const int nt = r16 ? 32 * BNW16 : 32 * BW_WARPS;
+        const int nt = r16 ? 32 * BNW16 : rmax <= (1ull << 24) ? 64 : 32;
         int per = 0, dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(bk, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bk, nt, 0) != cudaSuccess || per < 1) per = 1;
-        const u64 need = (p.nchunks + nt / 32 - 1) / (nt / 32), g = (u64)sms * per;
+        const u64 need = (p.nchunks + nt / 32 - 1) / (nt / 32) + 1, g = (u64)sms * per;   // + the scanner
         bk<<<(unsigned)(need < g ? need : g), nt, 0, cs>>>(a);
     }
     sp.end();

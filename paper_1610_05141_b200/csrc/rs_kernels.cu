@@ -140,166 +140,194 @@ __device__ __forceinline__ u64 ld_relaxed(const u64 *p)
 constexpr int BW_WARPS = 4;
 // positions buffered per chunk (mean <= n0 = 1024; u64 positions only for
 // chunk ranges above 2^24, where the buffer is smaller to fit 48 KB)
-// A warp takes a TICKET of G consecutive chunks (fewer look-back
-// participants, and look-back waits amortised over G chunks), buffers their
-// positions (type B, relative to each chunk start) in shared memory, looks
-// back over tickets, then stores.  T = position arithmetic (u32 while a
-// batch's 64 steps fit, else u64).
+// A warp takes a TICKET of G consecutive chunks and buffers their positions
+// (type B, relative to each chunk start) in shared memory.  Offsets come
+// from a single-pass look-back whose inclusive prefixes are produced IN
+// ORDER by one scanner warp (block 0, warp 0): generating warps only publish
+// their ticket's count (AGG), and -- double-buffered -- generate their next
+// ticket before they wait for the previous one's prefix (INC), so neither a
+// slow predecessor nor a long look-back walk stalls them.  T = position
+// arithmetic (u32 while a batch's 64 steps fit, else u64).
+template <typename T, typename B, int G, u32 CAP>
+__device__ __forceinline__ u32 bern_ticket(const BernArgs &a, u64 tk, B *bw, u32 (&cnt)[G], float c,
+                                           float m_abs, u32 lane, bool &overflow)
+{
+    u32 total = 0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        cnt[g] = 0;
+        const u64 ci = tk * G + g;
+        if (ci >= a.nchunks) continue;
+        const u64 gi = a.chunk0 + ci;
+        const u64 lo = bound_at(a.N, a.Db, gi);
+        const T r = (T)(bound_at(a.N, a.Db, gi + 1) - lo);
+        const u32 r32 = r > (T)0x7fffffffu ? 0x7fffffffu : (u32)r;    // fast path saturation point
+        const bool rfull = r <= (T)0x7fffffffu;
+        const Stream st(a.seed, P_GEO, ((u64)1 << a.Db) + gi);
+        B *bg = bw + total;
+        const u32 room = CAP - total;
+        // skips in batches of 64 draws: lane l has draws 2(q0 + l), 2(q0 + l) + 1
+        T S = 0;
+        u32 count = 0;
+        for (u32 q0 = 0;; q0 += 32) {
+            const u32x4 w = philox_rk(q0 + lane, st, a.rk);
+            bool ok0, ok1;
+            const u32 g0 = skip_fast(w.x, w.y, c, m_abs, r32, rfull, ok0);
+            const u32 g1 = skip_fast(w.z, w.w, c, m_abs, r32, rfull, ok1);
+            T s0 = (T)g0 + 1, s1 = (T)g1 + 1;
+            if (__any_sync(0xffffffffu, !(ok0 && ok1))) {      // rare: exact fp64 (CANON)
+                if (!ok0) s0 = skip_exact<T>(u52(w.x, w.y), a.log1m_rho, r);
+                if (!ok1) s1 = skip_exact<T>(u52(w.z, w.w), a.log1m_rho, r);
+            }
+            T incl = s0 + s1;                                  // inclusive scan over lanes
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const T y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= (u32)o) incl += y;
+            }
+            const T S1 = S + incl, S0 = S1 - s1;               // positions (relative) + 1
+            const u32 j0 = 2 * (q0 + lane);
+            if (S0 <= r) { if (j0 < room) bg[j0] = (B)(S0 - 1); else overflow = true; }
+            if (S1 <= r) { if (j0 + 1 < room) bg[j0 + 1] = (B)(S1 - 1); else overflow = true; }
+            const T tot = __shfl_sync(0xffffffffu, incl, 31);
+            const u32 e = __popc(__ballot_sync(0xffffffffu, S0 <= r)) +
+                          __popc(__ballot_sync(0xffffffffu, S1 <= r));
+            count += e;
+            if (e < 64) break;
+            S += tot;
+        }
+        if (__any_sync(0xffffffffu, overflow)) count = min(count, room);
+        cnt[g] = count;
+        total += count;
+    }
+    return total;
+}
+
+template <typename B, int G>
+__device__ __forceinline__ void bern_write(const BernArgs &a, u64 tk, const B *bw, const u32 (&cnt)[G],
+                                           u64 excl, u32 lane)
+{
+    u32 off = 0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const u64 ci = tk * G + g;
+        if (ci >= a.nchunks) break;
+        const u64 base = bound_at(a.N, a.Db, a.chunk0 + ci) + 1;
+        u64 *o = a.out + excl + off;
+        const u64 cap = a.capacity > excl + off ? a.capacity - (excl + off) : 0;
+        for (u32 i = lane; i < cnt[g]; i += 32)
+            if (i < cap) o[i] = base + (u64)bw[off + i];
+        off += cnt[g];
+    }
+}
+
+constexpr u64 B_AGG = 1ull << 62, B_INC = 2ull << 62, B_VAL = (1ull << 62) - 1;
+
+// The scanner: turns the published ticket counts (AGG) into inclusive
+// prefixes (INC) in ticket order, 256 tickets per step.
+__device__ __forceinline__ void bern_scanner(const BernArgs &a, u64 ntick, u32 lane)
+{
+    u64 next = 0, run = 0;
+    while (next < ntick) {
+        u64 v[8];
+        u32 fu = 8;                                    // first unpublished entry of the lane
+#pragma unroll
+        for (int i = 7; i >= 0; --i) {
+            const u64 idx = next + 8 * lane + i;
+            v[i] = idx < ntick ? ld_relaxed(a.status + idx) : 0ull;
+            if (idx >= ntick || (v[i] >> 62) == 0) fu = i;
+        }
+        const u32 first = __reduce_min_sync(0xffffffffu, fu == 8 ? 0xffffffffu : 8 * lane + fu);
+        const u32 np = first == 0xffffffffu ? 256u : first;   // consecutive published tickets
+        if (np == 0) { __nanosleep(256); continue; }
+        u64 loc = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) if (8 * lane + i < np) loc += v[i] & B_VAL;
+        u64 incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u64 y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (u32)o) incl += y;
+        }
+        u64 pref = run + incl - loc;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (8 * lane + i < np) {
+                pref += v[i] & B_VAL;
+                st_relaxed(a.status + next + 8 * lane + i, B_INC | pref);
+            }
+        }
+        run += __shfl_sync(0xffffffffu, incl, 31);
+        next += np;
+    }
+    if (lane == 0) *a.count_dev = run;
+}
+
+__device__ __forceinline__ u64 bern_wait_inc(const BernArgs &a, u64 tk)
+{
+    u64 v = ld_relaxed(a.status + tk);
+    while ((v >> 62) != 2) {
+        __nanosleep(128);
+        v = ld_relaxed(a.status + tk);
+    }
+    return v & B_VAL;
+}
+
 template <typename T, typename B, int G, u32 CAP, int NW>
 __device__ __forceinline__ void bernoulli_chunks(const BernArgs &a)
 {
-    __shared__ B buf[NW][CAP];
+    __shared__ B buf[NW][2][CAP];
     const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    B *bw = buf[wid];
+    const u64 ntick = (a.nchunks + G - 1) / G;
+    if (blockIdx.x == 0 && wid == 0) { bern_scanner(a, ntick, lane); return; }
     const float c = (float)(0x1.62e42fefa39efp-1 / a.log1m_rho);   // ln 2 / lr
     const float m_abs = (float)(0x1p-19 / -a.log1m_rho) + 0x1p-20f;
-    const u64 AGG = 1ull << 62, INC = 2ull << 62, VAL = (1ull << 62) - 1;
-    const u64 ntick = (a.nchunks + G - 1) / G;
+    bool overflow = false, have_prev = false;
+    u32 cur = 0, prev_cnt[G], prev_total = 0;
+    u64 prev_tk = 0;
     for (;;) {
         u32 tk = 0;
         if (lane == 0) tk = atomicAdd(a.ticket, 1u);
         tk = __shfl_sync(0xffffffffu, tk, 0);
-        if (tk >= ntick) break;
-        u32 cnt[G];
-        u32 total = 0;
-        bool overflow = false;
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            cnt[g] = 0;
-            const u64 ci = (u64)tk * G + g;
-            if (ci >= a.nchunks) continue;
-            const u64 gi = a.chunk0 + ci;
-            const u64 lo = bound_at(a.N, a.Db, gi);
-            const T r = (T)(bound_at(a.N, a.Db, gi + 1) - lo);
-            const u32 r32 = r > (T)0x7fffffffu ? 0x7fffffffu : (u32)r;    // fast path saturation point
-            const bool rfull = r <= (T)0x7fffffffu;
-            const Stream st(a.seed, P_GEO, ((u64)1 << a.Db) + gi);
-            B *bg = bw + total;
-            const u32 room = CAP - total;
-            // skips in batches of 64 draws: lane l has draws 2(q0 + l), 2(q0 + l) + 1
-            T S = 0;
-            u32 count = 0;
-            for (u32 q0 = 0;; q0 += 32) {
-                const u32x4 w = philox_rk(q0 + lane, st, a.rk);
-                bool ok0, ok1;
-                const u32 g0 = skip_fast(w.x, w.y, c, m_abs, r32, rfull, ok0);
-                const u32 g1 = skip_fast(w.z, w.w, c, m_abs, r32, rfull, ok1);
-                T s0 = (T)g0 + 1, s1 = (T)g1 + 1;
-                if (__any_sync(0xffffffffu, !(ok0 && ok1))) {  // rare: exact fp64 (CANON)
-                    if (!ok0) s0 = skip_exact<T>(u52(w.x, w.y), a.log1m_rho, r);
-                    if (!ok1) s1 = skip_exact<T>(u52(w.z, w.w), a.log1m_rho, r);
-                }
-                T incl = s0 + s1;                              // inclusive scan over lanes
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const T y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= (u32)o) incl += y;
-                }
-                const T S1 = S + incl, S0 = S1 - s1;           // positions (relative) + 1
-                const u32 j0 = 2 * (q0 + lane);
-                if (S0 <= r) { if (j0 < room) bg[j0] = (B)(S0 - 1); else overflow = true; }
-                if (S1 <= r) { if (j0 + 1 < room) bg[j0 + 1] = (B)(S1 - 1); else overflow = true; }
-                const T tot = __shfl_sync(0xffffffffu, incl, 31);
-                const u32 e = __popc(__ballot_sync(0xffffffffu, S0 <= r)) +
-                              __popc(__ballot_sync(0xffffffffu, S1 <= r));
-                count += e;
-                if (e < 64) break;
-                S += tot;
+        if (tk < ntick) {
+            u32 cnt[G];
+            const u32 total = bern_ticket<T, B, G, CAP>(a, tk, buf[wid][cur], cnt, c, m_abs, lane, overflow);
+            if (lane == 0) st_relaxed(a.status + tk, B_AGG | total);
+            if (have_prev) {                                       // the previous ticket's prefix
+                const u64 excl = bern_wait_inc(a, prev_tk) - prev_total;
+                __syncwarp();
+                bern_write<B, G>(a, prev_tk, buf[wid][cur ^ 1], prev_cnt, excl, lane);
             }
-            if (__any_sync(0xffffffffu, overflow)) count = min(count, room);
-            cnt[g] = count;
-            total += count;
-        }
-        if (__any_sync(0xffffffffu, overflow) && lane == 0) atomicOr(&g_rs_errors, 2u);
-        // decoupled look-back over tickets: status words (flag << 62 | value),
-        // relaxed gpu-scope accesses (each word carries its own value).  A lane
-        // reads four predecessors (128 per step); only predecessors nearer
-        // than the nearest inclusive one need to be published.
-        u64 excl = 0;
-#ifdef RS_EXP_NOLOOKBACK
-        excl = (u64)tk * G * 600;
-        if (true) {
-        } else
-#endif
-        if (tk == 0) {
-            if (lane == 0) st_relaxed(a.status, INC | total);
+#pragma unroll
+            for (int g = 0; g < G; ++g) prev_cnt[g] = cnt[g];
+            prev_total = total;
+            prev_tk = tk;
+            have_prev = true;
+            cur ^= 1;
+            __syncwarp();
         } else {
-            if (lane == 0) st_relaxed(a.status + tk, AGG | total);
-            long long p = (long long)tk - 1;
-            u64 v[4];
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const long long idx = p - (long long)(4 * lane + t);
-                v[t] = idx >= 0 ? ld_relaxed(a.status + idx) : (INC | 0ull);
+            if (have_prev) {
+                const u64 excl = bern_wait_inc(a, prev_tk) - prev_total;
+                __syncwarp();
+                bern_write<B, G>(a, prev_tk, buf[wid][cur ^ 1], prev_cnt, excl, lane);
             }
-            for (;;) {
-                u32 dinc = 0xffffffffu, dpen = 0xffffffffu;
-#pragma unroll
-                for (int t = 3; t >= 0; --t) {
-                    if ((v[t] >> 62) == 2) dinc = 4 * lane + t;
-                    if ((v[t] >> 62) == 0) dpen = 4 * lane + t;
-                }
-                dinc = __reduce_min_sync(0xffffffffu, dinc);
-                dpen = __reduce_min_sync(0xffffffffu, dpen);
-                if (dpen < dinc) {                          // a nearer predecessor is not published yet
-#ifndef RS_BSLEEP
-#define RS_BSLEEP 2000
-#endif
-                    __nanosleep(RS_BSLEEP);                 // yield issue slots to generating warps
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const long long idx = p - (long long)(4 * lane + t);
-                        if ((v[t] >> 62) == 0 && 4 * lane + t < dinc) v[t] = ld_relaxed(a.status + idx);
-                    }
-                    continue;
-                }
-                u64 add = 0;
-#pragma unroll
-                for (int t = 0; t < 4; ++t)
-                    if (4 * lane + t <= dinc) add += v[t] & VAL;   // dinc = ~0: all 128
-#pragma unroll
-                for (int o = 16; o; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
-                excl += add;
-                if (dinc != 0xffffffffu) break;
-                p -= 128;
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const long long idx = p - (long long)(4 * lane + t);
-                    v[t] = idx >= 0 ? ld_relaxed(a.status + idx) : (INC | 0ull);
-                }
-            }
-            if (lane == 0) st_relaxed(a.status + tk, INC | (excl + total));
+            break;
         }
-        if (lane == 0 && tk == ntick - 1) *a.count_dev = excl + total;
-        __syncwarp();
-        u32 off = 0;
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const u64 ci = (u64)tk * G + g;
-            if (ci >= a.nchunks) break;
-            const u64 base = bound_at(a.N, a.Db, a.chunk0 + ci) + 1;
-            u64 *o = a.out + excl + off;
-            const u64 cap = a.capacity > excl + off ? a.capacity - (excl + off) : 0;
-            for (u32 i = lane; i < cnt[g]; i += 32)
-                if (i < cap) o[i] = base + (u64)bw[off + i];
-            off += cnt[g];
-        }
-        __syncwarp();
     }
+    if (__any_sync(0xffffffffu, overflow) && lane == 0) atomicOr(&g_rs_errors, 2u);
 }
 
-// chunk range r <= 2^16: u16 positions, 4 chunks per ticket (4864 x 2 B per warp)
 #ifndef RS_BG
-#define RS_BG 4
+#define RS_BG 2
 #endif
 constexpr int BG16 = RS_BG;                                           // chunks per ticket (u16 path)
 constexpr u32 BCAP16 = ((BG16 * 1024 + 10 * 32 * (BG16 < 4 ? 2 : BG16 / 2) + 63) / 64) * 64;
-constexpr int BNW16 = (BCAP16 * 2 * 4 <= 48 * 1024) ? 4 : (BCAP16 * 2 * 2 <= 48 * 1024) ? 2 : 1;
+constexpr int BNW16 = (BCAP16 * 2 * 2 * 4 <= 48 * 1024) ? 4 : (BCAP16 * 2 * 2 * 2 <= 48 * 1024) ? 2 : 1;
 __global__ void __launch_bounds__(32 * BNW16) k_bernoulli(BernArgs a) { bernoulli_chunks<u32, uint16_t, BG16, BCAP16, BNW16>(a); }
 // r <= 2^24: u32 positions, 2 chunks per ticket (2560 x 4 B per warp)
-__global__ void __launch_bounds__(32 * BW_WARPS) k_bernoulli32(BernArgs a) { bernoulli_chunks<u32, u32, 2, 2560, BW_WARPS>(a); }
+__global__ void __launch_bounds__(64) k_bernoulli32(BernArgs a) { bernoulli_chunks<u32, u32, 2, 2560, 2>(a); }
 // larger r: u64 positions, 1 chunk per ticket (1536 x 8 B per warp)
-__global__ void __launch_bounds__(32 * BW_WARPS) k_bernoulli64(BernArgs a) { bernoulli_chunks<u64, u64, 1, 1536, BW_WARPS>(a); }
+__global__ void __launch_bounds__(32) k_bernoulli64(BernArgs a) { bernoulli_chunks<u64, u64, 1, 1536, 1>(a); }
 
 // ===========================================================================
 // Validation helpers.

@@ -160,8 +160,8 @@ struct BernArgs {
 };
 
 __global__ void k_bernoulli(BernArgs a);                           // chunk ranges <= 2^16
-__global__ void __launch_bounds__(128) k_bernoulli32(BernArgs a);   // chunk ranges <= 2^24
-__global__ void __launch_bounds__(128) k_bernoulli64(BernArgs a);   // larger chunk ranges
+__global__ void k_bernoulli32(BernArgs a);                         // chunk ranges <= 2^24
+__global__ void k_bernoulli64(BernArgs a);                         // larger chunk ranges
 
 // Validation (tests / bench correctness checks).
 __global__ void k_digest(const u64 *v, u64 n, u64 base, u64 *acc);
