@@ -59,6 +59,8 @@ constexpr u32 WL_SENT0 = 0xFFFFFFFFu - (u32)WL_CAP;   // sentinel at position p:
 
 struct WarpLeaf {
     u32 cnt[WL_B + WL_B / 32];             // padded bucket counters / starts (33 words per lane)
+    unsigned long long pf_off;             // prefetched count / offset of the warp's next leaf
+    u32 pf_k, pf_pad;                      //   (in shared memory: not live in registers)
     u32 keys[WL_CAP];                      // staging (draw order), then positions: pad, draws, sentinels
 };
 
@@ -430,14 +432,24 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
     __syncwarp();
     const u64 stride = (u64)gridDim.x * WL_WARPS;
     u64 L = (u64)blockIdx.x * WL_WARPS + wid;
-    u32 k_next = L < a.nleaves ? a.cnt[L] : 0u;
-    u64 off_next = L < a.nleaves ? a.off[L] : 0ull;
+    // the next leaf's count / offset arrive by cp.async straight into shared
+    // memory while this leaf is processed (no register stays live for them)
+    const u32 s_k = (u32)__cvta_generic_to_shared(&sh.pf_k), s_off = (u32)__cvta_generic_to_shared(&sh.pf_off);
+    if (lane == 0 && L < a.nleaves) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s_k), "l"(a.cnt + L) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s_off), "l"(a.off + L) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     for (; L < a.nleaves; L += stride) {
-        const u32 k = k_next;
-        const u64 off = off_next;
-        if (L + stride < a.nleaves) {          // prefetch the next leaf's count and offset
-            k_next = a.cnt[L + stride];
-            off_next = a.off[L + stride];
+        if (lane == 0) asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        const u32 k = sh.pf_k;
+        const u64 off = sh.pf_off;
+        __syncwarp();
+        if (lane == 0 && L + stride < a.nleaves) {   // prefetch the next leaf's count and offset
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s_k), "l"(a.cnt + L + stride) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s_off), "l"(a.off + L + stride) : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
         }
         if (k == 0) continue;
         const LeafGeom g = leaf_geom(a, L);
