@@ -136,6 +136,8 @@ def _max_over_ranks(x, world, device):
     if world == 1:
         return x
     import torch.distributed as dist
+    if dist.get_backend() != "nccl":
+        device = torch.device("cpu")
     t = torch.tensor([x], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -216,11 +218,16 @@ def run_reference(args):
 def run_native(args):
     import paper_1610_05141_b200 as rs
     world, rank, local = _dist()
+    local = local % max(torch.cuda.device_count(), 1)   # (gloo smoke test: ranks may share a GPU)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")   # collective tensors
     wl = _workload(args.workload, world)
     mode = wl["mode"]
     stream = torch.cuda.current_stream()
@@ -239,17 +246,17 @@ def run_native(args):
         def step():
             rs.bernoulli_ws(N, rho, seed, world, rank, out, local_cap, cnt, ws)
             if world > 1:
-                allc = torch.empty(world, dtype=torch.int64, device=dev)
-                dist.all_gather_into_tensor(allc, cnt.view(torch.int64))
+                allc = torch.empty(world, dtype=torch.int64, device=cdev)
+                dist.all_gather_into_tensor(allc, cnt.view(torch.int64).to(cdev))
     else:
         N, n, seed = wl["N"], wl["n"], wl["seed"]
         m = rs.MODE_WR if mode == "wr" else rs.MODE_WOR
         n_local, g_off = rs.shard_info(N, n, seed, world, rank, m)
         out = torch.empty(max(n_local, 1), dtype=torch.uint64, device=dev)
         ws = torch.empty(rs.workspace_bytes(m, N, n, 0.0, world), dtype=torch.uint8, device=dev)
-        cnt = torch.tensor([n_local], dtype=torch.int64, device=dev)
+        cnt = torch.tensor([n_local], dtype=torch.int64, device=cdev)
         fn = rs.sample_wr_ws if m == rs.MODE_WR else rs.sample_wor_ws
-        allc = torch.empty(world, dtype=torch.int64, device=dev)
+        allc = torch.empty(world, dtype=torch.int64, device=cdev)
 
         def step():
             fn(N, n, seed, world, rank, out, ws)
@@ -302,7 +309,7 @@ def run_native(args):
     if not args.no_check:
         assert bad == 0, f"validation failed: {bad} bad values"
         assert rs.device_errors(clear=True) == 0, "device capacity flag raised"
-    total = torch.tensor([n_local_done], dtype=torch.float64, device=dev)
+    total = torch.tensor([n_local_done], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(total)
     n_total = float(total.item())
@@ -411,6 +418,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-check", action="store_true", help="dev: skip the output validation asserts")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: smoke-test the N > 1 path with ranks sharing one GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
