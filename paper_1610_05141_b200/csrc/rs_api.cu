@@ -206,11 +206,18 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         a.root_cnt = p.root_cnt; a.root_off = 0;        // offsets local to the shard
         if (p.s + p.top == p.D) { a.leaf_cnt = leaf_cnt; a.leaf_off = leaf_off; }
         else { a.out_cnt = ping_cnt; a.out_off = ping_off; }
-        k_split<<<1, SPLIT_NT, 0, st>>>(a);
+        (a.wr ? k_split_wr : k_split)<<<1, SPLIT_NT, 0, st>>>(a);
         ++t_launches;
     }
     const u64 *in_cnt = ping_cnt, *in_off = ping_off;
-    for (int d = p.s + p.top; d < p.D; ++d) {         // one launch per deeper level
+    // the last NL levels (when there are level kernels at all) in one launch,
+    // a thread per depth-(D-NL) subtree
+#ifndef RS_SPLIT_DEEP
+#define RS_SPLIT_DEEP 3
+#endif
+    const int below = p.D - p.s - p.top;               // levels after the top CTA
+    const int NL = below >= RS_SPLIT_DEEP + 1 ? RS_SPLIT_DEEP : 0;
+    for (int d = p.s + p.top; d < p.D - NL; ++d) {    // one launch per level
         LevelArgs a;
         memset(&a, 0, sizeof a);
         a.N = p.N; a.seed = p.seed; a.wr = (p.mode == RS_MODE_WR); a.d = d;
@@ -222,9 +229,24 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         if (d + 1 == p.D) { a.leaf_cnt = leaf_cnt; a.leaf_off = leaf_off; }
         else { a.out_cnt = oc; a.out_off = oo; }
         const u64 grid = (a.width + LEVEL_NT - 1) / LEVEL_NT;
-        k_split_level<<<(unsigned)grid, LEVEL_NT, 0, st>>>(a);
+        (a.wr ? k_split_level_wr : k_split_level)<<<(unsigned)grid, LEVEL_NT, 0, st>>>(a);
         ++t_launches;
         in_cnt = oc; in_off = oo;
+    }
+    if (NL) {
+        LevelArgs a;
+        memset(&a, 0, sizeof a);
+        const int d = p.D - NL;
+        a.N = p.N; a.seed = p.seed; a.wr = (p.mode == RS_MODE_WR); a.d = d;
+        a.width = 1ull << (d - p.s);
+        a.node0 = p.idx << (d - p.s);
+        a.in_cnt = in_cnt; a.in_off = in_off;
+        a.leaf_cnt = leaf_cnt; a.leaf_off = leaf_off;
+        const u64 grid = (a.width + LEVEL_NT - 1) / LEVEL_NT;
+        void (*dk)(LevelArgs) = a.wr ? (NL == 2 ? k_split_deep2_wr : NL == 3 ? k_split_deep3_wr : k_split_deep4_wr)
+                                     : (NL == 2 ? k_split_deep2 : NL == 3 ? k_split_deep3 : k_split_deep4);
+        dk<<<(unsigned)grid, LEVEL_NT, 0, st>>>(a);
+        ++t_launches;
     }
     sp_split.end();
     Span sp_leaf(1, st);

@@ -9,7 +9,8 @@ __device__ unsigned g_rs_errors = 0;
 // ===========================================================================
 // Split tree (rows a3/a4).
 // ===========================================================================
-__global__ void __launch_bounds__(SPLIT_NT) k_split(SplitArgs a)
+template <bool WR>
+__device__ __forceinline__ void split_top(const SplitArgs &a)
 {
     __shared__ u64 buf[2][SPLIT_WIDTH];
     __shared__ u64 wtmp[SPLIT_NT / 32];
@@ -25,7 +26,7 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split(SplitArgs a)
         const u64 base = node << l;
         for (u32 j = tid; j < width; j += SPLIT_NT) {
             const u64 k = buf[cur][j];
-            const u64 x = split_node(a.wr != 0, a.N, d, base + j, k, a.seed);
+            const u64 x = split_node_t<WR>(a.N, d, base + j, k, a.seed);
             buf[cur ^ 1][2 * j] = x;
             buf[cur ^ 1][2 * j + 1] = k - x;
         }
@@ -56,12 +57,13 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split(SplitArgs a)
     }
 }
 
-__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_level(LevelArgs a)
+template <bool WR>
+__device__ __forceinline__ void split_level(const LevelArgs &a)
 {
     const u64 j = (u64)blockIdx.x * LEVEL_NT + threadIdx.x;
     if (j >= a.width) return;
     const u64 k = a.in_cnt[j], off = a.in_off[j];
-    const u64 x = split_node(a.wr != 0, a.N, a.d, a.node0 + j, k, a.seed);
+    const u64 x = split_node_t<WR>(a.N, a.d, a.node0 + j, k, a.seed);
     if (a.leaf_cnt) {
         if (k > 0xffffffffull) atomicOr(&g_rs_errors, 1u);
         a.leaf_cnt[2 * j] = (u32)x;
@@ -75,6 +77,57 @@ __global__ void __launch_bounds__(LEVEL_NT, 4) k_split_level(LevelArgs a)
         a.out_off[2 * j + 1] = off + x;
     }
 }
+
+// The last NL levels in one launch: thread j expands node (d, node0 + j)
+// through NL levels (2^NL - 1 deviates, breadth-first in registers) and
+// writes its 2^NL leaves.  Each lane now runs 2^NL - 1 rejection loops, so a
+// warp's slowest lane is close to its average (the divergence of one HRUA
+// loop per thread is averaged out), and NL - 1 global round trips and
+// launches disappear.
+template <int NL, bool WR>
+__device__ __forceinline__ void split_deep(const LevelArgs &a)
+{
+    const u64 j = (u64)blockIdx.x * LEVEL_NT + threadIdx.x;
+    if (j >= a.width) return;
+    constexpr int W = 1 << NL;
+    u64 c[W], o[W];
+    c[0] = a.in_cnt[j];
+    o[0] = a.in_off[j];
+    if (c[0] > 0xffffffffull * (u64)W) atomicOr(&g_rs_errors, 1u);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+        const int d = a.d + l;
+#pragma unroll
+        for (int i = (1 << l) - 1; i >= 0; --i) {          // in place, from the right
+            const u64 k = c[i], off = o[i];
+            const u64 x = split_node_t<WR>(a.N, d, ((a.node0 + j) << l) + i, k, a.seed);
+            c[2 * i] = x;
+            c[2 * i + 1] = k - x;
+            o[2 * i] = off;
+            o[2 * i + 1] = off + x;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        if (c[i] > 0xffffffffull) atomicOr(&g_rs_errors, 1u);
+        a.leaf_cnt[W * j + i] = (u32)c[i];
+        a.leaf_off[W * j + i] = o[i];
+    }
+}
+
+// WOR (hypergeometric) and WR (binomial) instantiations are separate
+// kernels: each holds only its deviate's code (the split kernels are
+// instruction-fetch bound).
+__global__ void __launch_bounds__(SPLIT_NT) k_split(SplitArgs a) { split_top<false>(a); }
+__global__ void __launch_bounds__(SPLIT_NT) k_split_wr(SplitArgs a) { split_top<true>(a); }
+__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_level(LevelArgs a) { split_level<false>(a); }
+__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_level_wr(LevelArgs a) { split_level<true>(a); }
+__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep2(LevelArgs a) { split_deep<2, false>(a); }
+__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep3(LevelArgs a) { split_deep<3, false>(a); }
+__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep4(LevelArgs a) { split_deep<4, false>(a); }
+__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep2_wr(LevelArgs a) { split_deep<2, true>(a); }
+__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep3_wr(LevelArgs a) { split_deep<3, true>(a); }
+__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep4_wr(LevelArgs a) { split_deep<4, true>(a); }
 
 }  // namespace rs
 

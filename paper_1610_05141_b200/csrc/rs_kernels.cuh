@@ -85,6 +85,7 @@ struct SplitArgs {
 };
 
 __global__ void __launch_bounds__(SPLIT_NT) k_split(SplitArgs a);
+__global__ void __launch_bounds__(SPLIT_NT) k_split_wr(SplitArgs a);
 
 // One tree level across the whole GPU: thread j splits node (d, node0 + j).
 constexpr int LEVEL_NT = 128;
@@ -99,6 +100,14 @@ struct LevelArgs {
     u64 *leaf_off;
 };
 __global__ void __launch_bounds__(LEVEL_NT, 4) k_split_level(LevelArgs a);
+__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_level_wr(LevelArgs a);
+// The last 2, 3 or 4 levels in one launch, a thread per subtree.
+__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep2(LevelArgs a);
+__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep3(LevelArgs a);
+__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep4(LevelArgs a);
+__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep2_wr(LevelArgs a);
+__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep3_wr(LevelArgs a);
+__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep4_wr(LevelArgs a);
 
 // ---------------------------------------------------------------------------
 // Leaf kernels (rows a5/a6/a7/a8).
