@@ -190,6 +190,12 @@ __device__ __forceinline__ u64 ld_relaxed(const u64 *p)
     return v;
 }
 
+__device__ __forceinline__ void st_v4b(u64 *p, u64 a, u64 b, u64 c, u64 d)
+{
+    asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d)
+                 : "memory");
+}
+
 constexpr int BW_WARPS = 4;
 // positions buffered per chunk (mean <= n0 = 1024; u64 positions only for
 // chunk ranges above 2^24, where the buffer is smaller to fit 48 KB)
@@ -217,41 +223,61 @@ __device__ __forceinline__ u32 bern_ticket(const BernArgs &a, u64 tk, B *bw, u32
         const u32 r32 = r > (T)0x7fffffffu ? 0x7fffffffu : (u32)r;    // fast path saturation point
         const bool rfull = r <= (T)0x7fffffffu;
         const Stream st(a.seed, P_GEO, ((u64)1 << a.Db) + gi);
-        B *bg = bw + total;
+        B *bg = bw + total;                        // 4-aligned (vector stores)
         const u32 room = CAP - total;
-        // skips in batches of 64 draws: lane l has draws 2(q0 + l), 2(q0 + l) + 1
+        // skips in batches of 128 draws: lane l has draws 4(q0 + l) .. +3,
+        // i.e. Philox blocks 2(q0 + l) and 2(q0 + l) + 1 (draw j = pair j mod 2
+        // of block j / 2, R3)
         T S = 0;
         u32 count = 0;
         for (u32 q0 = 0;; q0 += 32) {
-            const u32x4 w = philox_rk(q0 + lane, st, a.rk);
-            bool ok0, ok1;
-            const u32 g0 = skip_fast(w.x, w.y, c, m_abs, r32, rfull, ok0);
-            const u32 g1 = skip_fast(w.z, w.w, c, m_abs, r32, rfull, ok1);
-            T s0 = (T)g0 + 1, s1 = (T)g1 + 1;
-            if (__any_sync(0xffffffffu, !(ok0 && ok1))) {      // rare: exact fp64 (CANON)
-                if (!ok0) s0 = skip_exact<T>(u52(w.x, w.y), a.log1m_rho, r);
-                if (!ok1) s1 = skip_exact<T>(u52(w.z, w.w), a.log1m_rho, r);
+            const u32x4 w0 = philox_rk(2 * (q0 + lane), st, a.rk);
+            const u32x4 w1 = philox_rk(2 * (q0 + lane) + 1, st, a.rk);
+            bool ok0, ok1, ok2, ok3;
+            const u32 g0 = skip_fast(w0.x, w0.y, c, m_abs, r32, rfull, ok0);
+            const u32 g1 = skip_fast(w0.z, w0.w, c, m_abs, r32, rfull, ok1);
+            const u32 g2 = skip_fast(w1.x, w1.y, c, m_abs, r32, rfull, ok2);
+            const u32 g3 = skip_fast(w1.z, w1.w, c, m_abs, r32, rfull, ok3);
+            T s0 = (T)g0 + 1, s1 = (T)g1 + 1, s2 = (T)g2 + 1, s3 = (T)g3 + 1;
+            if (__any_sync(0xffffffffu, !(ok0 && ok1 && ok2 && ok3))) {   // rare: exact fp64 (CANON)
+                if (!ok0) s0 = skip_exact<T>(u52(w0.x, w0.y), a.log1m_rho, r);
+                if (!ok1) s1 = skip_exact<T>(u52(w0.z, w0.w), a.log1m_rho, r);
+                if (!ok2) s2 = skip_exact<T>(u52(w1.x, w1.y), a.log1m_rho, r);
+                if (!ok3) s3 = skip_exact<T>(u52(w1.z, w1.w), a.log1m_rho, r);
             }
-            T incl = s0 + s1;                                  // inclusive scan over lanes
+            const T l1 = s0 + s1, l2 = l1 + s2, l4 = l2 + s3;       // lane-local prefix
+            T incl = l4;                                           // inclusive scan over lanes
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const T y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= (u32)o) incl += y;
             }
-            const T S1 = S + incl, S0 = S1 - s1;               // positions (relative) + 1
-            const u32 j0 = 2 * (q0 + lane);
-            if (S0 <= r) { if (j0 < room) bg[j0] = (B)(S0 - 1); else overflow = true; }
-            if (S1 <= r) { if (j0 + 1 < room) bg[j0 + 1] = (B)(S1 - 1); else overflow = true; }
+            const T E = S + incl - l4;                             // before this lane's draws
+            const T S0 = E + s0, S1 = E + l1, S2 = E + l2, S3 = E + l4;   // positions + 1
+            const u32 j0 = 4 * (q0 + lane);
+            if (S3 <= r && j0 + 3 < room) {                        // all four (common)
+                if (sizeof(B) == 2) {
+                    const u32 lo2 = (u32)(S0 - 1) | ((u32)(S1 - 1) << 16), hi2 = (u32)(S2 - 1) | ((u32)(S3 - 1) << 16);
+                    *reinterpret_cast<uint2 *>(bg + j0) = make_uint2(lo2, hi2);
+                } else {
+                    bg[j0] = (B)(S0 - 1); bg[j0 + 1] = (B)(S1 - 1); bg[j0 + 2] = (B)(S2 - 1); bg[j0 + 3] = (B)(S3 - 1);
+                }
+            } else {
+                if (S0 <= r) { if (j0 < room) bg[j0] = (B)(S0 - 1); else overflow = true; }
+                if (S1 <= r) { if (j0 + 1 < room) bg[j0 + 1] = (B)(S1 - 1); else overflow = true; }
+                if (S2 <= r) { if (j0 + 2 < room) bg[j0 + 2] = (B)(S2 - 1); else overflow = true; }
+                if (S3 <= r) { if (j0 + 3 < room) bg[j0 + 3] = (B)(S3 - 1); else overflow = true; }
+            }
             const T tot = __shfl_sync(0xffffffffu, incl, 31);
-            const u32 e = __popc(__ballot_sync(0xffffffffu, S0 <= r)) +
-                          __popc(__ballot_sync(0xffffffffu, S1 <= r));
+            const u32 e = __popc(__ballot_sync(0xffffffffu, S0 <= r)) + __popc(__ballot_sync(0xffffffffu, S1 <= r)) +
+                          __popc(__ballot_sync(0xffffffffu, S2 <= r)) + __popc(__ballot_sync(0xffffffffu, S3 <= r));
             count += e;
-            if (e < 64) break;
+            if (e < 128) break;
             S += tot;
         }
         if (__any_sync(0xffffffffu, overflow)) count = min(count, room);
         cnt[g] = count;
-        total += count;
+        total += (count + 3) & ~3u;                // next chunk starts 4-aligned in the buffer
     }
     return total;
 }
@@ -260,17 +286,38 @@ template <typename B, int G>
 __device__ __forceinline__ void bern_write(const BernArgs &a, u64 tk, const B *bw, const u32 (&cnt)[G],
                                            u64 excl, u32 lane)
 {
-    u32 off = 0;
+    u32 off = 0, boff = 0;                                // output / buffer offsets of chunk g
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         const u64 ci = tk * G + g;
         if (ci >= a.nchunks) break;
         const u64 base = bound_at(a.N, a.Db, a.chunk0 + ci) + 1;
-        u64 *o = a.out + excl + off;
-        const u64 cap = a.capacity > excl + off ? a.capacity - (excl + off) : 0;
-        for (u32 i = lane; i < cnt[g]; i += 32)
-            if (i < cap) o[i] = base + (u64)bw[off + i];
-        off += cnt[g];
+        const u64 o0 = excl + off;                        // output index of this chunk's first value
+        const u32 n = cnt[g];
+        const u64 lim = a.capacity > o0 ? min(a.capacity - o0, (u64)n) : 0;
+        // groups of four on the output's 32-byte grid: group q covers chunk
+        // values i = 4q - h .. 4q - h + 3
+        const u32 h = (u32)(reinterpret_cast<uintptr_t>(a.out + o0) >> 3) & 3u;
+        u64 *d0 = a.out + (o0 - h);
+        const u32 ng = (u32)((h + lim + 3) >> 2);
+        for (u32 q = lane; q < ng; q += 32) {
+            const int i0 = (int)(4 * q) - (int)h;
+            u64 v[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int i = i0 + t;
+                v[t] = (i >= 0 && (u64)i < lim) ? base + (u64)bw[boff + i] : 0ull;
+            }
+            if (i0 >= 0 && (u64)(i0 + 4) <= lim) {
+                st_v4b(d0 + 4 * q, v[0], v[1], v[2], v[3]);
+            } else {
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (i0 + t >= 0 && (u64)(i0 + t) < lim) d0[4 * q + t] = v[t];
+            }
+        }
+        off += n;
+        boff += (n + 3) & ~3u;
     }
 }
 
@@ -344,7 +391,10 @@ __device__ __forceinline__ void bernoulli_chunks(const BernArgs &a)
         tk = __shfl_sync(0xffffffffu, tk, 0);
         if (tk < ntick) {
             u32 cnt[G];
-            const u32 total = bern_ticket<T, B, G, CAP>(a, tk, buf[wid][cur], cnt, c, m_abs, lane, overflow);
+            bern_ticket<T, B, G, CAP>(a, tk, buf[wid][cur], cnt, c, m_abs, lane, overflow);
+            u32 total = 0;
+#pragma unroll
+            for (int g = 0; g < G; ++g) total += cnt[g];
             if (lane == 0) st_relaxed(a.status + tk, B_AGG | total);
             if (have_prev) {                                       // the previous ticket's prefix
                 const u64 excl = bern_wait_inc(a, prev_tk) - prev_total;
