@@ -264,9 +264,9 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         // small leaf ranges: warp per leaf over a bitmap (complement or WOR)
         la.out_base = p.shard_lo;
         void (*bk)(LeafArgs) = p.comp ? k_leaf_bitmap_comp : k_leaf_bitmap_wor;
-        const size_t bsm = sizeof(BitmapLeaf) * WL_WARPS;
-        const unsigned gb = leaf_grid((const void *)bk, 32 * WL_WARPS, bsm, (p.nleaves + WL_WARPS - 1) / WL_WARPS);
-        bk<<<gb, 32 * WL_WARPS, bsm, st>>>(la);
+        const size_t bsm = sizeof(BitmapLeaf) * WB_WARPS;
+        const unsigned gb = leaf_grid((const void *)bk, 32 * WB_WARPS, bsm, (p.nleaves + WB_WARPS - 1) / WB_WARPS);
+        bk<<<gb, 32 * WB_WARPS, bsm, st>>>(la);
         ++t_launches;
         sp_leaf.end();
         return cuda_ok();

@@ -138,17 +138,20 @@ __global__ void __launch_bounds__(LEAF_NT) k_leaf_comp64(LeafArgs a);
 
 // Warp-per-leaf kernels (u32 keys): the common path; see rs_leaf.cuh.
 #ifndef RS_WL_MINB
-#define RS_WL_MINB 4
+#define RS_WL_MINB 1
 #endif
 #ifndef RS_WL_WARPS
-#define RS_WL_WARPS 4
+#define RS_WL_WARPS 16
 #endif
-constexpr int WL_WARPS = RS_WL_WARPS;            // warps (independent leaves) per CTA
+// warps (independent leaves) per CTA: measured best at 16 (one 16-warp CTA per
+// SM) for the counting-sort kernel and at 8 for the bitmap kernel
+constexpr int WL_WARPS = RS_WL_WARPS;
+constexpr int WB_WARPS = 8;
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr(LeafArgs a);
 // Warp-per-leaf bitmap kernels for leaf ranges r <= 2^15 (rs_leaf_bitmap.cuh).
-__global__ void __launch_bounds__(32 * WL_WARPS) k_leaf_bitmap_wor(LeafArgs a);
-__global__ void __launch_bounds__(32 * WL_WARPS) k_leaf_bitmap_comp(LeafArgs a);
+__global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_wor(LeafArgs a);
+__global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_comp(LeafArgs a);
 
 // ---------------------------------------------------------------------------
 // Bernoulli (row a9): one chunk per CTA (dynamic ticket order), geometric

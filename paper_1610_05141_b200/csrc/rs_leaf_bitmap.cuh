@@ -51,8 +51,8 @@ __device__ __forceinline__ void bitmap_leaves(const LeafArgs &a)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     BitmapLeaf &sh = reinterpret_cast<BitmapLeaf *>(smem_raw)[wid];
-    const u64 stride = (u64)gridDim.x * WL_WARPS;
-    for (u64 L = (u64)blockIdx.x * WL_WARPS + wid; L < a.nleaves; L += stride) {
+    const u64 stride = (u64)gridDim.x * WB_WARPS;
+    for (u64 L = (u64)blockIdx.x * WB_WARPS + wid; L < a.nleaves; L += stride) {
         const u32 k = a.cnt[L];                     // sample (WOR) or excluded (complement) count
         const LeafGeom g = leaf_geom(a, L);
         const u32 r = (u32)g.r;
@@ -130,7 +130,7 @@ __device__ __forceinline__ void bitmap_leaves(const LeafArgs &a)
     }
 }
 
-__global__ void __launch_bounds__(32 * WL_WARPS) k_leaf_bitmap_wor(LeafArgs a) { bitmap_leaves<false>(a); }
-__global__ void __launch_bounds__(32 * WL_WARPS) k_leaf_bitmap_comp(LeafArgs a) { bitmap_leaves<true>(a); }
+__global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_wor(LeafArgs a) { bitmap_leaves<false>(a); }
+__global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_comp(LeafArgs a) { bitmap_leaves<true>(a); }
 
 }  // namespace rs

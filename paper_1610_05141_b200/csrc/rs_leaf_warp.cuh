@@ -31,7 +31,7 @@
 // are appended to a spill list that the CTA kernel (rs_leaf.cuh) completes.
 
 #ifndef RS_WL_MINB
-#define RS_WL_MINB 4          // resident CTAs per SM the register budget is sized for
+#define RS_WL_MINB 1          // resident CTAs per SM the register budget is sized for (16 warps)
 #endif
 
 namespace rs {
