@@ -109,6 +109,19 @@ rs_status rs_node_info(int mode, uint64_t N, uint64_t n, uint64_t seed, int dept
 rs_status rs_sample_node(int mode, uint64_t N, uint64_t n, uint64_t seed, int depth,
                          uint64_t index, uint64_t *out, void *stream);
 
+/* ---- uneven universe (NEXT-2) ---------------------------------
+ * p PEs (GPUs, ranks) own L[0..p) elements ("owner computes"); the n
+ * samples of their union are assigned to the PEs by the paper's binomial
+ * tree: subtree sums of L bottom-up, then hypergeometric splits of the count
+ * top-down, the deviate of the subtree over PEs 2^j a .. keyed by that
+ * range (R13).  Host only (no device); every rank computes the
+ * same counts from the all-gathered L, so the paper's tree messages become
+ * one all-gather of p words.  n > sum L or sum L >= 2^63 -> RS_EINVAL.
+ * rs_uneven_seed: the seed of PE i's local sample, rs_sample_wor(L[i],
+ * counts[i], rs_uneven_seed(seed, i)) (values are local element indices). */
+rs_status rs_uneven_counts(int p, const uint64_t *L, uint64_t n, uint64_t seed, uint64_t *counts);
+uint64_t rs_uneven_seed(uint64_t seed, uint64_t pe);
+
 /* ---- caller-provided workspace variants --------------------------------
  * rs_workspace_bytes: bytes of device workspace the *_ws calls need for
  * (mode, N, n or rho, world).  ws must be 256-byte aligned.  Too small ->

@@ -81,6 +81,8 @@ def lib():
             "rso_small_samples": (None, [u64, u64, u64, u64, i32, P64]),
             "rso_digest_leaves_replay": (i32, [u64, u64, u64, i32, i32, u64, u64, P64, P64]),
             "rso_bern_chunks_digest": (i32, [u64, dbl, u64, u64, u64, P64, P64]),
+            "rso_uneven_counts": (i32, [i32, P64, u64, u64, P64]),
+            "rso_uneven_seed": (u64, [u64, u64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -289,3 +291,16 @@ def bern_chunks_digest(N, rho, seed, c_lo, c_hi):
     d, v = C.c_uint64(), C.c_uint64()
     _check(lib().rso_bern_chunks_digest(N, rho, seed, c_lo, c_hi, C.byref(d), C.byref(v)))
     return d.value, v.value
+
+
+def uneven_counts(L, n, seed):
+    """Per-PE sample counts for an uneven universe."""
+    Lv = np.ascontiguousarray(np.asarray(L, dtype=np.uint64))
+    out = np.zeros(Lv.size, dtype=np.uint64)
+    _check(lib().rso_uneven_counts(int(Lv.size), _p64(Lv), int(n), int(seed) % 2**64, _p64(out)))
+    return out
+
+
+def uneven_seed(seed, i):
+    return int(lib().rso_uneven_seed(int(seed) % 2**64, int(i)))
+

@@ -955,3 +955,59 @@ int rso_bern_chunks_digest(u64 N, double rho, u64 seed, u64 c_lo, u64 c_hi, u64 
     *digest = dig; *values = vals;
     return RSO_OK;
 }
+
+/* ------------------------------------------------------------------------
+ * NEXT-2: uneven universe (Section 4.3).  PE i owns L[i]
+ * elements.  "Arrange the processors into a binomial tree ... At level j we
+ * get (maximal) subtrees spanning processors 2^j a .. min(2^j a + 2^j - 1,
+ * p - 1)"; the L-values are summed bottom-up and the n samples are split
+ * top-down: "an inner node uses a hypergeometric distribution with
+ * parameters n [read: its n'], L_l and L_l + L_r to split its n' samples".
+ * "The subtree representing processors a..b can use this range as an input
+ * for the hash function h": the deviate of the level-j subtree a is keyed
+ * by its heap index 2^(J-j) + a (J = ceil log2 p) with bit 62 set (DESIGN
+ * R13: disjoint from every node id of the sampling tree).  A subtree whose
+ * right half is empty passes n' to the left without a deviate.  Written
+ * recursively, exactly as the paper's top-down pass. */
+static u64 sum_range(const u64 *L, int lo, int hi)
+{
+    u64 s = 0;
+    for (int i = lo; i < hi; i++) s += L[i];
+    return s;
+}
+
+static void uneven_rec(int p, int J, int j, u64 a, u64 nprime, const u64 *L, u64 seed, u64 *counts)
+{
+    const u64 lo = a << j;
+    if (j == 0) { counts[lo] = nprime; return; }
+    const u64 mid = lo + ((u64)1 << (j - 1));
+    if (mid >= (u64)p) { uneven_rec(p, J, j - 1, 2 * a, nprime, L, seed, counts); return; }
+    const u64 hi = lo + ((u64)1 << j) < (u64)p ? lo + ((u64)1 << j) : (u64)p;
+    const u64 Ll = sum_range(L, (int)lo, (int)mid), Lr = sum_range(L, (int)mid, (int)hi);
+    const u64 id = ((u64)1 << 62) | (((u64)1 << (J - j)) + a);
+    const u64 x = nprime == 0 ? 0 : rso_hgd(nprime, Ll, Ll + Lr, seed, id);
+    uneven_rec(p, J, j - 1, 2 * a, x, L, seed, counts);
+    uneven_rec(p, J, j - 1, 2 * a + 1, nprime - x, L, seed, counts);
+}
+
+/* counts[0..p) of the n samples; -1 if p < 1, n > sum L or sum L >= 2^63. */
+int rso_uneven_counts(int p, const u64 *L, u64 n, u64 seed, u64 *counts)
+{
+    if (p < 1) return -1;
+    u64 tot = 0;
+    for (int i = 0; i < p; i++) {
+        if (L[i] >= ((u64)1 << 63) - tot) return -1;
+        tot += L[i];
+    }
+    if (n > tot) return -1;
+    int J = 0;
+    while (((u64)1 << J) < (u64)p) J++;
+    uneven_rec(p, J, J, 0, n, L, seed, counts);
+    return 0;
+}
+
+/* Seed of PE i's local sample (DESIGN R13): mix64(seed + golden * (i + 1)). */
+u64 rso_uneven_seed(u64 seed, u64 i)
+{
+    return mix64(seed + 0x9E3779B97F4A7C15ull * (i + 1));
+}

@@ -54,6 +54,8 @@ SIGNATURES = {
     "rs_launch_count": (_u64, [_int]),
     "rs_set_option": (_int, [_int, _int]),
     "rs_node_info": (_int, [_int, _u64, _u64, _u64, _int, _u64, _P64, _P64]),
+    "rs_uneven_counts": (_int, [_int, _P64, _u64, _u64, _P64]),
+    "rs_uneven_seed": (_u64, [_u64, _u64]),
     "rs_sample_node": (_int, [_int, _u64, _u64, _u64, _int, _u64, _vp, _vp]),
     "rs_timing_enable": (_int, [_int]),
     "rs_timing_read": (_int, [_int, C.POINTER(_dbl), _P64]),
@@ -294,6 +296,26 @@ def sample_node(mode: int, N: int, n: int, seed: int, depth: int, index: int, ou
     _check(lib().rs_sample_node(int(mode), N, n, seed % 2**64, int(depth), int(index), _ptr(o),
                                 _stream(stream)))
     return o[:cnt]
+
+
+def uneven_counts(L, n: int, seed: int):
+    """Per-PE sample counts for PEs owning L[i] elements: a list."""
+    p = len(L)
+    La = (C.c_uint64 * p)(*[int(x) for x in L])
+    out = (C.c_uint64 * p)()
+    _check(lib().rs_uneven_counts(p, La, int(n), seed % 2**64, out))
+    return [int(v) for v in out]
+
+
+def uneven_seed(seed: int, pe: int) -> int:
+    return int(lib().rs_uneven_seed(seed % 2**64, int(pe)))
+
+
+def uneven_local_sample(L, n: int, seed: int, pe: int, device="cuda", stream=None):
+    """PE pe's share of a uniform n-subset of the union of all PEs' elements:
+    sorted local element indices (1-based) on the device, and its count."""
+    cnt = uneven_counts(L, n, seed)[pe]
+    return sample_wor(int(L[pe]), cnt, uneven_seed(seed, pe), device=device, stream=stream), cnt
 
 
 def leaf_range_nodes(D: int, lo: int, hi: int):

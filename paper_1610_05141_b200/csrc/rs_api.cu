@@ -548,6 +548,47 @@ rs_status rs_bernoulli_ws(uint64_t N, double rho, uint64_t seed, int world, int 
                          stream));
 }
 
+rs_status rs_uneven_counts(int p, const uint64_t *L, uint64_t n, uint64_t seed, uint64_t *counts)
+{
+    if (p < 1 || !L || !counts) return ret(RS_EINVAL);
+    // prefix sums of L (subtree sums are differences)
+    std::vector<u64> pre((size_t)p + 1, 0);
+    for (int i = 0; i < p; ++i) {
+        if (L[i] >= (1ull << 63) - pre[i]) return ret(RS_EINVAL);
+        pre[i + 1] = pre[i] + L[i];
+    }
+    if (n > pre[p]) return ret(RS_EINVAL);
+    int J = 0;
+    while ((1ull << J) < (u64)p) ++J;
+    // top-down, level by level: cur[a] = samples of the level-j subtree a
+    std::vector<u64> cur(1, n), nxt;
+    for (int j = J; j > 0; --j) {
+        nxt.assign(cur.size() * 2, 0);
+        for (size_t a = 0; a < cur.size(); ++a) {
+            const u64 lo = (u64)a << j, mid = lo + (1ull << (j - 1));
+            if (lo >= (u64)p) continue;
+            if (mid >= (u64)p) { nxt[2 * a] = cur[a]; continue; }     // no right half
+            const u64 hi = (lo + (1ull << j)) < (u64)p ? lo + (1ull << j) : (u64)p;
+            const u64 Ll = pre[mid] - pre[lo], Lt = pre[hi] - pre[lo];
+            const u64 id = (1ull << 62) | ((1ull << (J - j)) + a);
+            const u64 x = cur[a] ? hgd(cur[a], Ll, Lt, seed, id) : 0;
+            nxt[2 * a] = x;
+            nxt[2 * a + 1] = cur[a] - x;
+        }
+        cur.swap(nxt);
+    }
+    for (int i = 0; i < p; ++i) counts[i] = cur[(size_t)i];
+    return ret(RS_OK);
+}
+
+uint64_t rs_uneven_seed(uint64_t seed, uint64_t pe)
+{
+    u64 z = seed + 0x9E3779B97F4A7C15ull * (pe + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
 rs_status rs_node_info(int mode, uint64_t N, uint64_t n, uint64_t seed, int depth, uint64_t index,
                        uint64_t *count, uint64_t *global_offset)
 {

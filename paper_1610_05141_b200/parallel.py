@@ -68,3 +68,20 @@ def bernoulli(N: int, rho: float, seed: int, group=None, stream=None):
         raise RuntimeError("bernoulli shard: capacity exceeded")
     allc = allgather_counts(c, group, vals.device)
     return vals[:c], int(allc[:rank].sum().item())
+
+
+def uneven_sample(L_local: int, n: int, seed: int, group=None, stream=None):
+    """NEXT-2: every rank owns L_local elements; returns this
+    rank's sorted local element indices (1-based, device) of a uniform
+    n-subset of the union, plus (its count, all ranks' L).  The paper's
+    binomial-tree messages become one all-gather of the L values; each rank
+    then replays the whole count tree (rs_uneven_counts) -- every rank
+    derives the same counts."""
+    from . import uneven_local_sample
+    world, rank = _group_info(group)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    allL = allgather_counts(L_local, group, dev if dist.get_backend(group) == "nccl" else None)
+    L = [int(v) for v in allL.tolist()]
+    vals, cnt = uneven_local_sample(L, n, seed, rank, stream=stream)
+    return vals, cnt, L
+

@@ -144,3 +144,15 @@ def test_node_info_matches_oracle_replay(N, n, mode):
         rs.node_info(mode, N, n, 1, D + 1, 0)
     with pytest.raises(rs.RSError):
         rs.node_info(mode, N, n, 1, 2, 4)
+
+
+@pytest.mark.parametrize("L,n", [([17, 3, 40, 0, 25, 9, 11, 30, 14, 22, 8, 31, 19], 50),
+                                 ([2 ** 40, 5, 3 * 2 ** 33, 2 ** 20], 2 ** 30), ([7], 3),
+                                 ([1, 2, 3, 4, 5, 6, 7, 8], 36), ([0, 0, 5], 2)])
+def test_uneven_counts_match_oracle(L, n):
+    for seed in (1, 2 ** 64 - 1, 12345):
+        assert rs.uneven_counts(L, n, seed) == [int(v) for v in O.uneven_counts(L, n, seed)]
+    for i in range(len(L)):
+        assert rs.uneven_seed(seed, i) == O.uneven_seed(seed, i)
+    with pytest.raises(rs.RSError):
+        rs.uneven_counts(L, sum(L) + 1, 1)

@@ -264,3 +264,17 @@ def test_host_buffer_batched_overlap():
     d = rs.sample_wor(N, n, 5)
     assert torch.equal(h.view(torch.int64), d.cpu().view(torch.int64))
     _sampled_leaf_parity(d, N, n, 5, O.MODE_WOR, nsample=16)
+
+
+# ---- NEXT-2: uneven universe over PEs ---------------------------------
+
+@pytest.mark.parametrize("L,n", [([17, 3, 40, 0, 25, 9, 11, 30, 14, 22, 8, 31, 19], 50),
+                                 ([2 ** 30, 3 * 2 ** 28, 12345, 2 ** 31], 2 ** 21),
+                                 ([10 ** 6, 1, 5 * 10 ** 5, 7 * 10 ** 5 + 3], 10 ** 6)])
+def test_uneven_local_samples(L, n):
+    counts = rs.uneven_counts(L, n, 21)
+    assert sum(counts) == n
+    for pe in range(len(L)):
+        vals, cnt = rs.uneven_local_sample(L, n, 21, pe)
+        exp = O.sample_wor(L[pe], cnt, O.uneven_seed(21, pe))
+        assert np.array_equal(_np(vals), exp), pe

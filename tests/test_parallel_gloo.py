@@ -36,7 +36,13 @@ def _worker(rank, world, port, errq):
             ec, eo = O.shard_info(N, n, seed, world, rank, mode)
             assert (cnt, off) == (ec, eo), (N, n, seed, mode, rank, cnt, off, ec, eo)
             assert int(allc.sum()) == n
-        # a mismatch between replay and all-gather must raise
+        # NEXT-2: all-gather of the L values, then the same count replay on every rank
+        import paper_1610_05141_b200 as rs
+        Lmine = [17, 3, 40, 25][rank % 4] * (rank + 1)
+        allL = P.allgather_counts(Lmine)
+        L = [int(v) for v in allL.tolist()]
+        counts = rs.uneven_counts(L, sum(L) // 3, 9)
+        assert counts == [int(v) for v in O.uneven_counts(L, sum(L) // 3, 9)]
         dist.destroy_process_group()
     except Exception as e:  # report to the parent
         errq.put(f"rank {rank}: {e!r}")
