@@ -66,6 +66,8 @@ def _workload(name, world):
         return dict(W.CFG3B)
     if name == "wr":
         return dict(W.CFG4)
+    if name == "gnm":
+        return dict(W.GNM)
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -251,6 +253,8 @@ def run_native(args):
     else:
         N, n, seed = wl["N"], wl["n"], wl["seed"]
         m = rs.MODE_WR if mode == "wr" else rs.MODE_WOR
+        if mode == "gnm" and world > 1:
+            raise SystemExit("gnm: single GPU only")
         n_local, g_off = rs.shard_info(N, n, seed, world, rank, m)
         out = torch.empty(max(n_local, 1), dtype=torch.uint64, device=dev)
         ws = torch.empty(rs.workspace_bytes(m, N, n, 0.0, world), dtype=torch.uint8, device=dev)
@@ -259,7 +263,10 @@ def run_native(args):
         allc = torch.empty(world, dtype=torch.int64, device=cdev)
 
         def step():
-            fn(N, n, seed, world, rank, out, ws)
+            if mode == "gnm":
+                rs.gnm(wl["V"], n, seed, out=out)
+            else:
+                fn(N, n, seed, world, rank, out, ws)
             if world > 1:
                 dist.all_gather_into_tensor(allc, cnt)   # per-GPU counts -> global offsets
 
@@ -301,7 +308,7 @@ def run_native(args):
         bad = rs.validate(out[:c_local], N, strict=True)
         n_local_done = c_local
     else:
-        bad = rs.validate(out[:n_local], N, strict=(mode != "wr"))
+        bad = rs.validate(out[:n_local], 2 ** 64 - 1 if mode == "gnm" else N, strict=(mode != "wr"))
         n_local_done = n_local
         if world > 1:
             off = int(allc[:rank].sum().item())
@@ -334,7 +341,7 @@ def run_native(args):
         if mode == "wor" and r_max <= 2 ** 15:
             kname = "k_leaf_bitmap_comp" if comp else "k_leaf_bitmap_wor"
         else:
-            kname = "k_leaf_warp_wr" if mode == "wr" else "k_leaf_warp_wor"
+            kname = {"wr": "k_leaf_warp_wr", "gnm": "k_leaf_warp_gnm"}.get(mode, "k_leaf_warp_wor")
     kms_per = kms / max(kl, 1)
     achieved = bytes_per_launch / (kms_per / 1e3) / 1e9 if kms_per > 0 else None
     traffic = None
@@ -352,7 +359,7 @@ def run_native(args):
 
     # ---- end to end through the C ABI with a host buffer (fewer steps)
     e2e = None
-    if not args.no_e2e and mode != "bernoulli":
+    if not args.no_e2e and mode not in ("bernoulli", "gnm"):
         try:
             try:
                 host = torch.empty(max(n_local, 1), dtype=torch.uint64, pin_memory=True)

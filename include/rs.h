@@ -109,6 +109,21 @@ rs_status rs_node_info(int mode, uint64_t N, uint64_t n, uint64_t seed, int dept
 rs_status rs_sample_node(int mode, uint64_t N, uint64_t n, uint64_t seed, int depth,
                          uint64_t index, uint64_t *out, void *stream);
 
+/* ---- Erdos-Renyi random graphs (NEXT-3) -----------------------
+ * "Generating a random graph in the G(n,m) and G(n,p) model ... is equivalent
+ * to sampling from the n(n-1)/2 possible edges": the WOR / Bernoulli sample
+ * over edge indices, with the index -> (u, v) decode fused into the leaf
+ * stores.  Vertices 0..V-1, 2 <= V < 2^32; edge index e (lexicographic over
+ * pairs u < v) is stored as (u << 32) | v, so the output is the edge list in
+ * lexicographic order.  rs_gnm: m distinct edges into edges[0..m) (m > V(V-1)/2
+ * -> RS_EINVAL).  rs_gnp: each edge independently with probability p;
+ * capacity / count_dev as rs_bernoulli (capacity from
+ * rs_bernoulli_capacity(V(V-1)/2, p)).  Outputs equal the decoded
+ * rs_sample_wor / rs_bernoulli samples over 1..V(V-1)/2 with the same seed. */
+rs_status rs_gnm(uint64_t V, uint64_t m, uint64_t seed, uint64_t *edges, void *stream);
+rs_status rs_gnp(uint64_t V, double p, uint64_t seed, uint64_t *edges, uint64_t capacity,
+                 uint64_t *count_dev, void *stream);
+
 /* ---- uneven universe (NEXT-2) ---------------------------------
  * p PEs (GPUs, ranks) own L[0..p) elements ("owner computes"); the n
  * samples of their union are assigned to the PEs by the paper's binomial

@@ -83,6 +83,7 @@ def lib():
             "rso_bern_chunks_digest": (i32, [u64, dbl, u64, u64, u64, P64, P64]),
             "rso_uneven_counts": (i32, [i32, P64, u64, u64, P64]),
             "rso_uneven_seed": (u64, [u64, u64]),
+            "rso_edges": (None, [u64, P64, u64, P64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -303,4 +304,20 @@ def uneven_counts(L, n, seed):
 
 def uneven_seed(seed, i):
     return int(lib().rso_uneven_seed(int(seed) % 2**64, int(i)))
+
+
+def edges(V, values):
+    """Packed (u << 32) | v edges of 1-based edge indices (NEXT-3)."""
+    v = np.ascontiguousarray(np.asarray(values, dtype=np.uint64))
+    out = np.zeros(v.size, dtype=np.uint64)
+    lib().rso_edges(int(V), _p64(v), int(v.size), _p64(out))
+    return out
+
+
+def gnm(V, m, seed):
+    return edges(V, sample_wor(V * (V - 1) // 2, m, seed))
+
+
+def gnp(V, p, seed):
+    return edges(V, bernoulli(V * (V - 1) // 2, p, seed))
 

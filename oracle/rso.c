@@ -1011,3 +1011,27 @@ u64 rso_uneven_seed(u64 seed, u64 i)
 {
     return mix64(seed + 0x9E3779B97F4A7C15ull * (i + 1));
 }
+
+/* NEXT-3: edge index e (0-based, lexicographic over pairs u < v of
+ * 0..V-1; row u holds V-1-u edges) -> (u << 32) | v.  The plain definition:
+ * u = the largest row with S(u) = u(2V-u-1)/2 <= e, by integer binary search
+ * (the SPEC's method), v = e - S(u) + u + 1.  Applied to a 1-based
+ * sample over 1..V(V-1)/2 in place of values[i] - 1. */
+static unsigned __int128 edge_row_start(u64 V, u64 u)
+{
+    return (unsigned __int128)u * (2 * (unsigned __int128)V - u - 1) / 2;
+}
+
+void rso_edges(u64 V, const u64 *values, u64 count, u64 *out)
+{
+    for (u64 i = 0; i < count; i++) {
+        const u64 e = values[i] - 1;
+        u64 lo = 0, hi = V - 2;                  /* largest u in [lo, hi] with S(u) <= e */
+        while (lo < hi) {
+            const u64 mid = lo + (hi - lo + 1) / 2;
+            if (edge_row_start(V, mid) <= e) lo = mid; else hi = mid - 1;
+        }
+        const u64 v = (u64)(e - edge_row_start(V, lo)) + lo + 1;
+        out[i] = (lo << 32) | v;
+    }
+}

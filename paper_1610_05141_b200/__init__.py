@@ -56,6 +56,8 @@ SIGNATURES = {
     "rs_node_info": (_int, [_int, _u64, _u64, _u64, _int, _u64, _P64, _P64]),
     "rs_uneven_counts": (_int, [_int, _P64, _u64, _u64, _P64]),
     "rs_uneven_seed": (_u64, [_u64, _u64]),
+    "rs_gnm": (_int, [_u64, _u64, _u64, _vp, _vp]),
+    "rs_gnp": (_int, [_u64, _dbl, _u64, _vp, _u64, _vp, _vp]),
     "rs_sample_node": (_int, [_int, _u64, _u64, _u64, _int, _u64, _vp, _vp]),
     "rs_timing_enable": (_int, [_int]),
     "rs_timing_read": (_int, [_int, C.POINTER(_dbl), _P64]),
@@ -296,6 +298,34 @@ def sample_node(mode: int, N: int, n: int, seed: int, depth: int, index: int, ou
     _check(lib().rs_sample_node(int(mode), N, n, seed % 2**64, int(depth), int(index), _ptr(o),
                                 _stream(stream)))
     return o[:cnt]
+
+
+def gnm(V: int, m: int, seed: int, out=None, device="cuda", stream=None):
+    """G(V, m): m distinct edges as packed (u << 32) | v, lexicographic order."""
+    _require_cuda()
+    o = _out(m, out, device)
+    _check(lib().rs_gnm(V, m, seed % 2**64, _ptr(o), _stream(stream)))
+    return o[:m]
+
+
+def gnp(V: int, p: float, seed: int, capacity=None, out=None, device="cuda", stream=None):
+    """G(V, p): every edge with probability p, packed (u << 32) | v, sorted."""
+    _require_cuda()
+    N = V * (V - 1) // 2
+    cap = bernoulli_capacity(N, p) if capacity is None else capacity
+    o = _out(cap, out, device)
+    cnt = torch.zeros(1, dtype=torch.uint64, device=o.device)
+    _check(lib().rs_gnp(V, float(p), seed % 2**64, _ptr(o), cap, _ptr(cnt), _stream(stream)))
+    c = int(cnt.item())
+    if c > cap:
+        raise RSError("gnp: capacity exceeded")
+    return o[:c]
+
+
+def unpack_edges(e):
+    """(u, v) int64 tensors of packed edges."""
+    x = e.view(torch.int64)
+    return x >> 32, x & 0xFFFFFFFF
 
 
 def uneven_counts(L, n: int, seed: int):

@@ -102,6 +102,7 @@ struct TreePlan {
     u64 leaf0, nleaves;     // shard's leaves
     u64 r_max;              // largest leaf range
     u64 local_count, global_offset;
+    u64 gV;                 // graph calls: vertex count (outputs are packed edges)
     int top;                // levels expanded by the single top CTA
     // workspace layout
     size_t o_ping_cnt, o_ping_off, o_pong_cnt, o_pong_off, o_leaf_cnt, o_leaf_off, o_spill, bytes;
@@ -256,6 +257,7 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
     la.leaf0 = p.leaf0; la.nleaves = p.nleaves;
     la.cnt = leaf_cnt; la.off = leaf_off; la.out = out;
     la.rk = round_keys(p.seed);
+    la.gV = p.gV;
     const bool wide = p.r_max > 0xfffff000ull;    // u32 keys (below the warp kernel's sentinels)
     const bool wr = (p.mode == RS_MODE_WR);
     void (*kern)(LeafArgs);
@@ -263,7 +265,8 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
     if (p.r_max <= BM_RMAX && p.mode == RS_MODE_WOR && g_leaf_path == 0) {
         // small leaf ranges: warp per leaf over a bitmap (complement or WOR)
         la.out_base = p.shard_lo;
-        void (*bk)(LeafArgs) = p.comp ? k_leaf_bitmap_comp : k_leaf_bitmap_wor;
+        void (*bk)(LeafArgs) = p.gV ? (p.comp ? k_leaf_bitmap_comp_g : k_leaf_bitmap_wor_g)
+                                    : (p.comp ? k_leaf_bitmap_comp : k_leaf_bitmap_wor);
         const size_t bsm = sizeof(BitmapLeaf) * WB_WARPS;
         const unsigned gb = leaf_grid((const void *)bk, 32 * WB_WARPS, bsm, (p.nleaves + WB_WARPS - 1) / WB_WARPS);
         bk<<<gb, 32 * WB_WARPS, bsm, st>>>(la);
@@ -281,7 +284,7 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         la.spill_n = spill_n;
         la.spill = spill_n + 1;
         cudaMemsetAsync(spill_n, 0, 4, st);
-        void (*wk)(LeafArgs) = wr ? k_leaf_warp_wr : k_leaf_warp_wor;
+        void (*wk)(LeafArgs) = wr ? k_leaf_warp_wr : p.gV ? k_leaf_warp_gnm : k_leaf_warp_wor;
         const size_t wsm = sizeof(WarpLeaf) * WL_WARPS;
         const u64 wgrid = (p.nleaves + WL_WARPS - 1) / WL_WARPS;
         const unsigned g1 = leaf_grid((const void *)wk, 32 * WL_WARPS, wsm, wgrid);
@@ -380,16 +383,16 @@ rs_status plan_bern(u64 N, double rho, int world, int rank, BernPlan &p)
     return RS_OK;
 }
 
-__global__ void k_fill_range(u64 *out, u64 lo, u64 n, u64 cap, u64 *count)
+__global__ void k_fill_range(u64 *out, u64 lo, u64 n, u64 cap, u64 *count, u64 gV)
 {
     const u64 m = n < cap ? n : cap;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x)
-        out[i] = lo + i + 1;
+        out[i] = out_word(lo + i + 1, gV);
     if (blockIdx.x == 0 && threadIdx.x == 0) *count = n;
 }
 
 rs_status bern_call(u64 N, double rho, u64 seed, int world, int rank, u64 *out, u64 capacity,
-                    u64 *count_dev, void *ws, size_t ws_bytes, void *stream)
+                    u64 *count_dev, void *ws, size_t ws_bytes, void *stream, u64 gV = 0)
 {
     if (!have_device()) return RS_ECUDA;
     BernPlan p;
@@ -399,7 +402,7 @@ rs_status bern_call(u64 N, double rho, u64 seed, int world, int rank, u64 *out, 
     const cudaStream_t cs = S(stream);
     if (rho == 0.0 || N == 0 || rho == 1.0) {
         const u64 n = (rho == 0.0 || N == 0) ? 0 : p.shard_hi - p.shard_lo;
-        k_fill_range<<<n ? 1184 : 1, 256, 0, cs>>>(out, p.shard_lo, n, capacity, count_dev);
+        k_fill_range<<<n ? 1184 : 1, 256, 0, cs>>>(out, p.shard_lo, n, capacity, count_dev, gV);
         ++t_launches;
         return cuda_ok();
     }
@@ -420,11 +423,13 @@ rs_status bern_call(u64 N, double rho, u64 seed, int world, int rank, u64 *out, 
     a.ticket = (u32 *)(w + p.o_ticket);
     a.out = out; a.capacity = capacity; a.count_dev = count_dev;
     a.rk = round_keys(seed);
+    a.gV = gV;
     Span sp(2, cs);
     {
         const u64 rmax = (N >> p.Db) + ((N & ((1ull << p.Db) - 1)) != 0);   // largest chunk range
         const bool r16 = rmax <= (1ull << 16);
-        void (*bk)(BernArgs) = r16 ? k_bernoulli : rmax <= (1ull << 24) ? k_bernoulli32 : k_bernoulli64;
+        void (*bk)(BernArgs) = gV ? (r16 ? k_bernoulli_g : rmax <= (1ull << 24) ? k_bernoulli32_g : k_bernoulli64_g)
+                                  : (r16 ? k_bernoulli : rmax <= (1ull << 24) ? k_bernoulli32 : k_bernoulli64);
         const int nt = r16 ? 32 * BNW16 : rmax <= (1ull << 24) ? 64 : 32;
         int per = 0, dev = 0, sms = 148;
         cudaGetDevice(&dev);
@@ -546,6 +551,34 @@ rs_status rs_bernoulli_ws(uint64_t N, double rho, uint64_t seed, int world, int 
     if (!ws) return ret(RS_EINVAL);
     return ret(bern_call(N, rho, seed, world, rank, out_local, capacity, count_dev, ws, ws_bytes,
                          stream));
+}
+
+// NEXT-3: Erdos-Renyi graphs over the V(V-1)/2 possible edges.
+static bool edge_count(uint64_t V, uint64_t *N)
+{
+    if (V < 2 || V > 0xffffffffull) return false;
+    *N = (V & 1) ? V * ((V - 1) >> 1) : (V >> 1) * (V - 1);
+    return true;
+}
+
+rs_status rs_gnm(uint64_t V, uint64_t m, uint64_t seed, uint64_t *edges, void *stream)
+{
+    u64 N;
+    if (!edge_count(V, &N)) return ret(RS_EINVAL);
+    if (!have_device()) return ret(RS_ECUDA);
+    TreePlan p;
+    rs_status st = plan_tree(RS_MODE_WOR, N, m, seed, 1, 0, p);
+    if (st != RS_OK) return ret(st);
+    p.gV = V;
+    return ret(plan_call(p, edges, nullptr, 0, stream));
+}
+
+rs_status rs_gnp(uint64_t V, double p, uint64_t seed, uint64_t *edges, uint64_t capacity,
+                 uint64_t *count_dev, void *stream)
+{
+    u64 N;
+    if (!edge_count(V, &N)) return ret(RS_EINVAL);
+    return ret(bern_call(N, p, seed, 1, 0, edges, capacity, count_dev, nullptr, 0, stream, V));
 }
 
 rs_status rs_uneven_counts(int p, const uint64_t *L, uint64_t n, uint64_t seed, uint64_t *counts)

@@ -282,7 +282,16 @@ __device__ __forceinline__ u32 bern_ticket(const BernArgs &a, u64 tk, B *bw, u32
     return total;
 }
 
-template <typename B, int G>
+// Graph calls (NEXT-3): chunk values -> packed edges (edge_pack), lane-strided
+// 8-byte stores (coalesced), not unrolled, so the kernel holds one decode.
+template <typename B>
+__device__ __noinline__ void bern_store_edges(u64 *d, const B *bw, u32 lim, u64 base, u64 gV, u32 lane)
+{
+#pragma unroll 1
+    for (u32 i = lane; i < lim; i += 32) d[i] = edge_pack(gV, base - 1 + (u64)bw[i]);
+}
+
+template <typename B, int G, bool GR>
 __device__ __forceinline__ void bern_write(const BernArgs &a, u64 tk, const B *bw, const u32 (&cnt)[G],
                                            u64 excl, u32 lane)
 {
@@ -297,6 +306,12 @@ __device__ __forceinline__ void bern_write(const BernArgs &a, u64 tk, const B *b
         const u64 lim = a.capacity > o0 ? min(a.capacity - o0, (u64)n) : 0;
         // groups of four on the output's 32-byte grid: group q covers chunk
         // values i = 4q - h .. 4q - h + 3
+        if (GR) {                                         // graph calls: one decode site
+            bern_store_edges(a.out + o0, bw + boff, (u32)lim, base, a.gV, lane);
+            off += n;
+            boff += (n + 3) & ~3u;
+            continue;
+        }
         const u32 h = (u32)(reinterpret_cast<uintptr_t>(a.out + o0) >> 3) & 3u;
         u64 *d0 = a.out + (o0 - h);
         const u32 ng = (u32)((h + lim + 3) >> 2);
@@ -306,7 +321,7 @@ __device__ __forceinline__ void bern_write(const BernArgs &a, u64 tk, const B *b
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 const int i = i0 + t;
-                v[t] = (i >= 0 && (u64)i < lim) ? base + (u64)bw[boff + i] : 0ull;
+                v[t] = (i >= 0 && (u64)i < lim) ? out_word_t<GR>(base + (u64)bw[boff + i], a.gV) : 0ull;
             }
             if (i0 >= 0 && (u64)(i0 + 4) <= lim) {
                 st_v4b(d0 + 4 * q, v[0], v[1], v[2], v[3]);
@@ -373,7 +388,7 @@ __device__ __forceinline__ u64 bern_wait_inc(const BernArgs &a, u64 tk)
     return v & B_VAL;
 }
 
-template <typename T, typename B, int G, u32 CAP, int NW>
+template <typename T, typename B, int G, u32 CAP, int NW, bool GR>
 __device__ __forceinline__ void bernoulli_chunks(const BernArgs &a)
 {
     __shared__ B buf[NW][2][CAP];
@@ -399,7 +414,7 @@ __device__ __forceinline__ void bernoulli_chunks(const BernArgs &a)
             if (have_prev) {                                       // the previous ticket's prefix
                 const u64 excl = bern_wait_inc(a, prev_tk) - prev_total;
                 __syncwarp();
-                bern_write<B, G>(a, prev_tk, buf[wid][cur ^ 1], prev_cnt, excl, lane);
+                bern_write<B, G, GR>(a, prev_tk, buf[wid][cur ^ 1], prev_cnt, excl, lane);
             }
 #pragma unroll
             for (int g = 0; g < G; ++g) prev_cnt[g] = cnt[g];
@@ -412,7 +427,7 @@ __device__ __forceinline__ void bernoulli_chunks(const BernArgs &a)
             if (have_prev) {
                 const u64 excl = bern_wait_inc(a, prev_tk) - prev_total;
                 __syncwarp();
-                bern_write<B, G>(a, prev_tk, buf[wid][cur ^ 1], prev_cnt, excl, lane);
+                bern_write<B, G, GR>(a, prev_tk, buf[wid][cur ^ 1], prev_cnt, excl, lane);
             }
             break;
         }
@@ -426,11 +441,14 @@ __device__ __forceinline__ void bernoulli_chunks(const BernArgs &a)
 constexpr int BG16 = RS_BG;                                           // chunks per ticket (u16 path)
 constexpr u32 BCAP16 = ((BG16 * 1024 + 10 * 32 * (BG16 < 4 ? 2 : BG16 / 2) + 63) / 64) * 64;
 constexpr int BNW16 = (BCAP16 * 2 * 2 * 4 <= 48 * 1024) ? 4 : (BCAP16 * 2 * 2 * 2 <= 48 * 1024) ? 2 : 1;
-__global__ void __launch_bounds__(32 * BNW16) k_bernoulli(BernArgs a) { bernoulli_chunks<u32, uint16_t, BG16, BCAP16, BNW16>(a); }
+__global__ void __launch_bounds__(32 * BNW16) k_bernoulli(BernArgs a) { bernoulli_chunks<u32, uint16_t, BG16, BCAP16, BNW16, false>(a); }
+__global__ void __launch_bounds__(32 * BNW16) k_bernoulli_g(BernArgs a) { bernoulli_chunks<u32, uint16_t, BG16, BCAP16, BNW16, true>(a); }
 // r <= 2^24: u32 positions, 2 chunks per ticket (2560 x 4 B per warp)
-__global__ void __launch_bounds__(64) k_bernoulli32(BernArgs a) { bernoulli_chunks<u32, u32, 2, 2560, 2>(a); }
+__global__ void __launch_bounds__(64) k_bernoulli32(BernArgs a) { bernoulli_chunks<u32, u32, 2, 2560, 2, false>(a); }
+__global__ void __launch_bounds__(64) k_bernoulli32_g(BernArgs a) { bernoulli_chunks<u32, u32, 2, 2560, 2, true>(a); }
 // larger r: u64 positions, 1 chunk per ticket (1536 x 8 B per warp)
-__global__ void __launch_bounds__(32) k_bernoulli64(BernArgs a) { bernoulli_chunks<u64, u64, 1, 1536, 1>(a); }
+__global__ void __launch_bounds__(32) k_bernoulli64(BernArgs a) { bernoulli_chunks<u64, u64, 1, 1536, 1, false>(a); }
+__global__ void __launch_bounds__(32) k_bernoulli64_g(BernArgs a) { bernoulli_chunks<u64, u64, 1, 1536, 1, true>(a); }
 
 // ===========================================================================
 // Validation helpers.

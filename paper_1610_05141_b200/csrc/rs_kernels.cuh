@@ -127,6 +127,7 @@ struct LeafArgs {
     const u32 *list;       // CTA kernel: if set, process only list[0 .. *list_n)
     const u32 *list_n;
     RoundKeys rk;          // Philox round keys of seed (round_keys(seed))
+    u64 gV;                // != 0: graph calls, store packed edges of G(gV, .) (NEXT-3)
 };
 
 __global__ void __launch_bounds__(LEAF_NT) k_leaf_wor32(LeafArgs a);
@@ -149,9 +150,12 @@ constexpr int WL_WARPS = RS_WL_WARPS;
 constexpr int WB_WARPS = 8;
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr(LeafArgs a);
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm(LeafArgs a);
 // Warp-per-leaf bitmap kernels for leaf ranges r <= 2^15 (rs_leaf_bitmap.cuh).
 __global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_wor(LeafArgs a);
 __global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_comp(LeafArgs a);
+__global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_wor_g(LeafArgs a);
+__global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_comp_g(LeafArgs a);
 
 // ---------------------------------------------------------------------------
 // Bernoulli (row a9): one chunk per CTA (dynamic ticket order), geometric
@@ -169,11 +173,15 @@ struct BernArgs {
     u64 capacity;
     u64 *count_dev;
     RoundKeys rk;          // Philox round keys of seed
+    u64 gV;                // != 0: graph calls, store packed edges (NEXT-3)
 };
 
 __global__ void k_bernoulli(BernArgs a);                           // chunk ranges <= 2^16
 __global__ void k_bernoulli32(BernArgs a);                         // chunk ranges <= 2^24
 __global__ void k_bernoulli64(BernArgs a);                         // larger chunk ranges
+__global__ void k_bernoulli_g(BernArgs a);                         // G(n, p) variants (NEXT-3)
+__global__ void k_bernoulli32_g(BernArgs a);
+__global__ void k_bernoulli64_g(BernArgs a);
 
 // Validation (tests / bench correctness checks).
 __global__ void k_digest(const u64 *v, u64 n, u64 base, u64 *acc);

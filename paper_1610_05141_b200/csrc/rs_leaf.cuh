@@ -329,7 +329,7 @@ __device__ __forceinline__ void load4(const u64 *p, u64 &a, u64 &b, u64 &c, u64 
 // dst[i] = base + keys[h + i], i < k; dst - h is 32-byte aligned, so whole
 // groups go out as 32-byte vector stores (row a6).
 template <typename K>
-__device__ __forceinline__ void store_run(const K *keys, u32 k, u32 h, u64 base, u64 *dst)
+__device__ __forceinline__ void store_run(const K *keys, u32 k, u32 h, u64 base, u64 *dst, u64 gV = 0)
 {
     u64 *d0 = dst - h;
     const u32 ng = (h + k + 3) >> 2;
@@ -338,11 +338,12 @@ __device__ __forceinline__ void store_run(const K *keys, u32 k, u32 h, u64 base,
         load4(keys + 4 * g, v[0], v[1], v[2], v[3]);
         const int i0 = (int)(4 * g) - (int)h;
         if (i0 >= 0 && i0 + 4 <= (int)k) {
-            st_v4(d0 + 4 * g, base + v[0], base + v[1], base + v[2], base + v[3]);
+            st_v4(d0 + 4 * g, out_word(base + v[0], gV), out_word(base + v[1], gV), out_word(base + v[2], gV),
+                  out_word(base + v[3], gV));
         } else {
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-                if (i0 + j >= 0 && i0 + j < (int)k) d0[4 * g + j] = base + v[j];
+                if (i0 + j >= 0 && i0 + j < (int)k) d0[4 * g + j] = out_word(base + v[j], gV);
         }
     }
 }
@@ -424,7 +425,7 @@ __device__ __forceinline__ void sample_leaves(const LeafArgs &a)
             else if (threadIdx.x == 0) atomicOr(&g_rs_errors, 1u);
         } else {
             const u32 h = (u32)(reinterpret_cast<uintptr_t>(dst) >> 3) & 3u;
-            if (leaf_sorted<K, WR>(sh, st, g.r, k, h)) store_run<K>(sh.keys, k, h, g.lo + 1, dst);
+            if (leaf_sorted<K, WR>(sh, st, g.r, k, h)) store_run<K>(sh.keys, k, h, g.lo + 1, dst, a.gV);
         }
         __syncthreads();
         zero_words(sh.W, LB_MAX);
@@ -504,7 +505,7 @@ __device__ __forceinline__ void complement_leaves(const LeafArgs &a)
             const u32 valid = (w + 1) * 32 <= nv ? 0xffffffffu : ((1u << (nv & 31)) - 1u);
             const u32 cw = ~sh.bm[w] & valid;
             if ((cw >> lane) & 1u)
-                dst[sh.wpre[w] + __popc(cw & ((1u << lane) - 1u))] = base + 32 * w + lane;
+                dst[sh.wpre[w] + __popc(cw & ((1u << lane) - 1u))] = out_word(base + 32 * w + lane, a.gV);
         }
         __syncthreads();
     }

@@ -45,7 +45,7 @@ __device__ __forceinline__ u32 bm_valid(u32 w, u32 r)
     return (w + 1) * 32 <= r ? 0xffffffffu : ((1u << (r & 31u)) - 1u);
 }
 
-template <bool COMP>
+template <bool COMP, bool GR>
 __device__ __forceinline__ void bitmap_leaves(const LeafArgs &a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -94,16 +94,16 @@ __device__ __forceinline__ void bitmap_leaves(const LeafArgs &a)
                 const u32 b2 = COMP ? ~W4.z : W4.z, b3 = COMP ? ~W4.w : W4.w;
                 const u32 p0 = pos, p1 = p0 + __popc(b0), p2 = p1 + __popc(b1), p3 = p2 + __popc(b2);
                 pos = p3 + __popc(b3);
-                if ((b0 >> lane) & 1u) dst[p0 + __popc(b0 & lm)] = vb;
-                if ((b1 >> lane) & 1u) dst[p1 + __popc(b1 & lm)] = vb + 32;
-                if ((b2 >> lane) & 1u) dst[p2 + __popc(b2 & lm)] = vb + 64;
-                if ((b3 >> lane) & 1u) dst[p3 + __popc(b3 & lm)] = vb + 96;
+                if ((b0 >> lane) & 1u) dst[p0 + __popc(b0 & lm)] = out_word_t<GR>(vb, a.gV);
+                if ((b1 >> lane) & 1u) dst[p1 + __popc(b1 & lm)] = out_word_t<GR>(vb + 32, a.gV);
+                if ((b2 >> lane) & 1u) dst[p2 + __popc(b2 & lm)] = out_word_t<GR>(vb + 64, a.gV);
+                if ((b3 >> lane) & 1u) dst[p3 + __popc(b3 & lm)] = out_word_t<GR>(vb + 96, a.gV);
             }
 #pragma unroll 1
             for (; w < nw; ++w, vb += 32) {
                 const u32 word = sh.bm[w];
                 const u32 bits = COMP ? (~word & bm_valid(w, r)) : word;
-                if ((bits >> lane) & 1u) dst[pos + __popc(bits & lm)] = vb;
+                if ((bits >> lane) & 1u) dst[pos + __popc(bits & lm)] = out_word_t<GR>(vb, a.gV);
                 pos += __popc(bits);
             }
         } else {
@@ -122,7 +122,7 @@ __device__ __forceinline__ void bitmap_leaves(const LeafArgs &a)
                 while (bits) {
                     const u32 b = __ffs(bits) - 1;
                     bits &= bits - 1;
-                    dst[pos++] = base + 32u * w + b;
+                    dst[pos++] = out_word_t<GR>(base + 32u * w + b, a.gV);
                 }
             }
         }
@@ -130,7 +130,9 @@ __device__ __forceinline__ void bitmap_leaves(const LeafArgs &a)
     }
 }
 
-__global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_wor(LeafArgs a) { bitmap_leaves<false>(a); }
-__global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_comp(LeafArgs a) { bitmap_leaves<true>(a); }
+__global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_wor(LeafArgs a) { bitmap_leaves<false, false>(a); }
+__global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_comp(LeafArgs a) { bitmap_leaves<true, false>(a); }
+__global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_wor_g(LeafArgs a) { bitmap_leaves<false, true>(a); }
+__global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_comp_g(LeafArgs a) { bitmap_leaves<true, true>(a); }
 
 }  // namespace rs

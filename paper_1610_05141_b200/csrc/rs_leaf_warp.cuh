@@ -292,9 +292,19 @@ __device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const RoundKeys &K, con
 
 // Steps 4-6 for E positions per lane.  Returns 0 (leaf stored) or, for WOR
 // with too few distinct values, the next round's draw count J' > J.
-template <int E, bool WR>
+// Graph calls (NEXT-3): positions [h, h + k) of sh.keys hold the leaf's
+// sorted offsets; decode each to its packed edge (edge_pack, rs_math.cuh) in a
+// non-unrolled loop so the kernel holds a single copy of the decode.
+__device__ __noinline__ void wl_store_edges(const WarpLeaf &sh, u64 *d0, u32 h, u32 k, u64 base, u64 gV, u32 lane)
+{
+#pragma unroll 1
+    for (u32 i = h + lane; i < h + k; i += 32) d0[i] = edge_pack(gV, base - 1 + sh.keys[i]);
+    __syncwarp();
+}
+
+template <int E, bool WR, bool GR>
 __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 P_, u64 base,
-                                         u64 *dst, u32 lane)
+                                         u64 *dst, u32 lane, u64 gV)
 {
     u32 P = P_;
     RS_TS(tf0);
@@ -370,17 +380,19 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
                     if (p >= h && p < h + J && !(p > h && y[i] == (i ? y[i - 1] : prv))) sh.keys[o++] = y[i];
                 }
                 __syncwarp();
+                if (GR) { wl_store_edges(sh, d0, h, k, base, gV, lane); return 0; }
                 const u32 ng = (h + k + 3) >> 2;
                 for (u32 g = lane; g < ng; g += 32) {
                     const uint4 t = *reinterpret_cast<const uint4 *>(&sh.keys[4 * g]);
                     const u32 vv[4] = {t.x, t.y, t.z, t.w};
                     const u32 i0 = 4 * g;
                     if (i0 >= h && i0 + 4 <= h + k) {
-                        st_v4(d0 + i0, base + vv[0], base + vv[1], base + vv[2], base + vv[3]);
+                        st_v4(d0 + i0, out_word_t<GR>(base + vv[0], gV), out_word_t<GR>(base + vv[1], gV),
+                              out_word_t<GR>(base + vv[2], gV), out_word_t<GR>(base + vv[3], gV));
                     } else {
 #pragma unroll
                         for (int t2 = 0; t2 < 4; ++t2)
-                            if (i0 + t2 >= h && i0 + t2 < h + k) d0[i0 + t2] = base + vv[t2];
+                            if (i0 + t2 >= h && i0 + t2 < h + k) d0[i0 + t2] = out_word_t<GR>(base + vv[t2], gV);
                     }
                 }
                 __syncwarp();
@@ -397,15 +409,28 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
     if (y[0] == 0x12345u && y[E-1] == 7u) d0[lane] = y[3];
     return 0;
 #endif
+    if (GR) {                                      // graph calls: packed edges
+        // one decode site: the sorted draws go through shared memory (16-byte
+        // stores, lane stride 4 (mod 32) banks: conflict-free per quarter
+        // warp), then lane-strided 8-byte stores (coalesced)
+        __syncwarp();
 #pragma unroll
-    for (int m = 0; m < E; m += 4) {
-        const u32 p = p0 + m;
-        st_v4_base_if(p >= h && p + 4 <= end, d0 + p, base, y[m], y[m + 1], y[m + 2], y[m + 3]);
+        for (int m = 0; m < E; m += 4)
+            *reinterpret_cast<uint4 *>(&sh.keys[p0 + m]) = make_uint4(y[m], y[m + 1], y[m + 2], y[m + 3]);
+        __syncwarp();
+        wl_store_edges(sh, d0, h, k, base, gV, lane);
+        return 0;
+    } else {
+#pragma unroll
+        for (int m = 0; m < E; m += 4) {
+            const u32 p = p0 + m;
+            st_v4_base_if(p >= h && p + 4 <= end, d0 + p, base, y[m], y[m + 1], y[m + 2], y[m + 3]);
+        }
     }
     if (lane == 0 && (h || end < 4)) {             // head group (positions 0..3) if partial
 #pragma unroll
         for (int t = 0; t < 4; ++t)
-            if ((u32)t >= h && (u32)t < end) d0[t] = base + y[t];
+            if ((u32)t >= h && (u32)t < end) d0[t] = out_word_t<GR>(base + y[t], gV);
     }
     const u32 tg = (end - 1) & ~3u;               // tail group start (if partial, and not the head)
     if ((end & 3u) && tg >= 4 && lane == tg / E) {
@@ -415,14 +440,14 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
             if ((u32)m == mt) {
 #pragma unroll
                 for (int t = 0; t < 3; ++t)
-                    if (tg + t < end) d0[tg + t] = base + y[m + t];
+                    if (tg + t < end) d0[tg + t] = out_word_t<GR>(base + y[m + t], gV);
             }
     }
     __syncwarp();
     return 0;
 }
 
-template <bool WR>
+template <bool WR, bool GR>
 __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -472,7 +497,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
                     wl_scatter(sh, a.rk, dr, J, h, shb, lane);
                     RS_TS(ts1);
                     RS_ACC(2, ts0, ts1);
-                    res = wl_finish<WL_E1, WR>(sh, J, k, h, P, base, dst, lane);
+                    res = wl_finish<WL_E1, WR, GR>(sh, J, k, h, P, base, dst, lane, a.gV);
                     RS_TS(ts2);
                     RS_ACC(5, ts1, ts2);
                 } else {
@@ -481,7 +506,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
                     __syncwarp();
 #else
                     wl_scatter(sh, a.rk, dr, J, h, shb, lane);
-                    res = wl_finish<WL_E2, WR>(sh, J, k, h, P, base, dst, lane);
+                    res = wl_finish<WL_E2, WR, GR>(sh, J, k, h, P, base, dst, lane, a.gV);
 #endif
                 }
             }
@@ -495,7 +520,9 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
     }
 }
 
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor(LeafArgs a) { warp_leaves<false>(a); }
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr(LeafArgs a) { warp_leaves<true>(a); }
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor(LeafArgs a) { warp_leaves<false, false>(a); }
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr(LeafArgs a) { warp_leaves<true, false>(a); }
+// G(n, m) (NEXT-3): the WOR kernel with the edge decode fused into its stores
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm(LeafArgs a) { warp_leaves<false, true>(a); }
 
 }  // namespace rs

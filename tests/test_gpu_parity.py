@@ -278,3 +278,28 @@ def test_uneven_local_samples(L, n):
         vals, cnt = rs.uneven_local_sample(L, n, 21, pe)
         exp = O.sample_wor(L[pe], cnt, O.uneven_seed(21, pe))
         assert np.array_equal(_np(vals), exp), pe
+
+
+# ---- NEXT-3: random graphs, decode fused into every store path --------------------
+
+@pytest.mark.parametrize("V,m", [(4, 6), (100, 37), (1000, 4000), (3000, 3 * 10 ** 6),     # warp / bitmap / complement
+                                 (2 ** 20 + 7, 2 ** 20), (70000, 2 ** 31)])
+def test_gnm(V, m):
+    got = _np(rs.gnm(V, m, 13))
+    assert np.array_equal(got, O.gnm(V, m, 13)), (V, m)
+    _no_device_errors()
+
+
+def test_gnm_cta_path():
+    rs.set_option(rs.OPT_LEAF_PATH, 1)
+    try:
+        got = _np(rs.gnm(5000, 10 ** 5, 2))
+    finally:
+        rs.set_option(rs.OPT_LEAF_PATH, 0)
+    assert np.array_equal(got, O.gnm(5000, 10 ** 5, 2))
+
+
+@pytest.mark.parametrize("V,p", [(5, 1.0), (1000, 0.01), (3000, 0.3), (2 ** 16, 1e-4)])
+def test_gnp(V, p):
+    got = _np(rs.gnp(V, p, 17))
+    assert np.array_equal(got, O.gnp(V, p, 17)), (V, p)
