@@ -2,7 +2,7 @@
 """Benchmark of the B200 divide-and-conquer sampler (arXiv 1610.05141).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
-                    [--workload headline|cfg1|cfg0|complement|bernoulli|wr]
+                    [--workload headline|cfg1|cfg0|complement|bernoulli|wr|gnm|algb]
 
 One "step" = one pass of the whole hot path over one sample: the split tree,
 the leaves and the stores, plus, for N > 1, the NCCL
@@ -68,6 +68,8 @@ def _workload(name, world):
         return dict(W.CFG4)
     if name == "gnm":
         return dict(W.GNM)
+    if name == "algb":
+        return dict(W.ALGB)
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -166,6 +168,14 @@ def oracle_sample(wl, target_s=10.0, leaf_start=0):
         return dict(value=v / dt, unit=UNIT, cores=1, kind="oracle",
                     sample=f"first {chunks} of {nch} Bernoulli chunks of {wl['name']} ({v} values, "
                            f"{dt:.1f} s, single-threaded oracle)")
+    if wl["mode"] == "algb":          # whole Algorithm B runs at a reduced n
+        N, ns = wl["N"], 2 ** 14
+        t = time.perf_counter(); O.algb(N, ns, wl["seed"], wl["slack"]); dt = time.perf_counter() - t
+        while dt < target_s / 4 and ns < wl["n"]:
+            ns *= 4
+            t = time.perf_counter(); O.algb(N, ns, wl["seed"], wl["slack"]); dt = time.perf_counter() - t
+        return dict(value=ns / dt, unit=UNIT, cores=1, kind="oracle",
+                    sample=f"whole Algorithm B at n={ns} of N={N} ({dt:.1f} s, single-threaded oracle)")
     mode = O.MODE_WR if wl["mode"] == "wr" else O.MODE_WOR
     N, n = wl["N"], wl["n"]
     D = O.plan(N, n, mode)[0]
@@ -250,6 +260,16 @@ def run_native(args):
             if world > 1:
                 allc = torch.empty(world, dtype=torch.int64, device=cdev)
                 dist.all_gather_into_tensor(allc, cnt.view(torch.int64).to(cdev))
+    elif mode == "algb":
+        N, n, seed = wl["N"], wl["n"], wl["seed"]
+        if world > 1:
+            raise SystemExit("algb: single GPU only (comparison baseline)")
+        m, n_local, g_off = rs.MODE_WOR, n, 0
+        out = torch.empty(n, dtype=torch.uint64, device=dev)
+        ws = torch.empty(rs.algb_workspace_bytes(N, n, wl["slack"]), dtype=torch.uint8, device=dev)
+
+        def step():
+            rs.sample_wor_algb(N, n, seed, slack=wl["slack"], out=out, ws=ws)
     else:
         N, n, seed = wl["N"], wl["n"], wl["seed"]
         m = rs.MODE_WR if mode == "wr" else rs.MODE_WOR
@@ -331,6 +351,18 @@ def run_native(args):
         nunits = 1 << (rs.plan(rs.MODE_BERNOULLI, N, 0, rho)[0])
         bytes_per_launch = 8.0 * n_local_done + 8.0 * nunits / world
         kname = "k_bernoulli"
+    elif mode == "algb":               # dominant of the Bernoulli pass and the compaction
+        rho = min(1.0, (n + wl["slack"] * math.sqrt(n)) / N)
+        npr = n + wl["slack"] * math.sqrt(n)                  # E[n'] (the pass count is host-side)
+        kb, kc = kt["bernoulli"], kt["other"]
+        if kb[0] >= kc[0]:
+            kms, kl = kb
+            bytes_per_launch = 8.0 * npr + 8.0 * (1 << rs.plan(rs.MODE_BERNOULLI, N, 0, rho)[0])
+            kname = "k_bernoulli64d"
+        else:
+            kms, kl = kc
+            bytes_per_launch = 8.0 * npr + 8.0 * n
+            kname = "k_algb_compact"
     else:
         kms, kl = kt["leaf"]
         D = rs.plan(m, N, n)[0]
@@ -355,11 +387,12 @@ def run_native(args):
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "kernel": kname, "kernel_ms": kms_per, "peak_source": peak_src,
                 "step_share": kms / max(args.steps, 1) / ms if ms > 0 else None,
-                "split_ms": kt["split"][0] / max(args.steps, 1)}
+                "split_ms": kt["split"][0] / max(args.steps, 1),
+                "classes_ms": {k: v[0] / max(args.steps, 1) for k, v in kt.items()}}
 
     # ---- end to end through the C ABI with a host buffer (fewer steps)
     e2e = None
-    if not args.no_e2e and mode not in ("bernoulli", "gnm"):
+    if not args.no_e2e and mode not in ("bernoulli", "gnm", "algb"):
         try:
             try:
                 host = torch.empty(max(n_local, 1), dtype=torch.uint64, pin_memory=True)

@@ -37,7 +37,8 @@ typedef enum {
     RS_EINVAL = 1,     /* invalid argument (n > N, rho not in [0,1], ...) */
     RS_ECUDA = 2,      /* CUDA runtime error / no device                  */
     RS_ENOMEM = 3,     /* workspace allocation failed / too small         */
-    RS_ECAPACITY = 4   /* output capacity exceeded (Bernoulli)            */
+    RS_ECAPACITY = 4,  /* output capacity exceeded (Bernoulli)            */
+    RS_EATTEMPTS = 5   /* Algorithm B: restart budget exhausted           */
 } rs_status;
 
 enum { RS_MODE_WOR = 0, RS_MODE_WR = 1, RS_MODE_BERNOULLI = 2 };
@@ -124,6 +125,28 @@ rs_status rs_gnm(uint64_t V, uint64_t m, uint64_t seed, uint64_t *edges, void *s
 rs_status rs_gnp(uint64_t V, double p, uint64_t seed, uint64_t *edges, uint64_t capacity,
                  uint64_t *count_dev, void *stream);
 
+/* ---- Algorithm B + repair (NEXT-4, the comparison baseline) -------------
+ * The paper's own GPU design B_GPU, composed from the
+ * kernels above: a Bernoulli sample with rho' = min(1, (n + slack sqrt(n)) /
+ * N) ("rho somewhat larger than n/N"), restarted with seed_a = seed + a *
+ * 0x9E3779B97F4A7C15 (a = 1, 2, ...) while its size n' < n ("simply restart"),
+ * then repaired by removing the elements at the n' - n positions of the WOR
+ * sample rs_sample_wor(n', n' - n, seed_a) ("Algorithm R to generate n'-n
+ * samples from the range 0..n'-1"), with a compaction kernel.  out: device,
+ * capacity >= n; receives n distinct values of 1..N, ascending -- a uniform
+ * n-subset, but NOT the same one as rs_sample_wor.  attempts (host, may be
+ * NULL): Bernoulli passes used.  Synchronous: n' goes to the host after every
+ * pass (as in the paper).  Workspace: ws (device, caller-owned)
+ * of ws_bytes >= rs_algb_workspace_bytes(N, n, slack) -- the Bernoulli buffer
+ * of rs_bernoulli_capacity(N, rho') values and the removal positions -- or
+ * ws = NULL: cudaMallocAsync / cudaFreeAsync on the stream.  n > N, slack < 0
+ * or not finite, N >= 2^63 -> RS_EINVAL; too small ws -> RS_ENOMEM; more
+ * than max_attempts passes -> RS_EATTEMPTS. */
+rs_status rs_sample_wor_algb(uint64_t N, uint64_t n, uint64_t seed, double slack,
+                             uint32_t max_attempts, uint64_t *out, uint32_t *attempts,
+                             void *ws, size_t ws_bytes, void *stream);
+uint64_t rs_algb_workspace_bytes(uint64_t N, uint64_t n, double slack);   /* 0 if invalid or n == 0 */
+
 /* ---- uneven universe (NEXT-2) ---------------------------------
  * p PEs (GPUs, ranks) own L[0..p) elements ("owner computes"); the n
  * samples of their union are assigned to the PEs by the paper's binomial
@@ -200,7 +223,7 @@ uint64_t rs_launch_count(int reset);
 
 /* Device-time instrumentation for benchmarks: while enabled, every call
  * records CUDA events on its launch stream around each kernel class
- * (0 split tree, 1 leaf, 2 Bernoulli, 3 other).  rs_timing_read
+ * (0 split tree, 1 leaf, 2 Bernoulli, 3 other: Algorithm B's compaction).  rs_timing_read
  * synchronises on the recorded events and returns the accumulated
  * milliseconds and launch counts per class (arrays of 4); reset != 0
  * clears them.  Disabled by default (no events recorded). */

@@ -84,6 +84,7 @@ def lib():
             "rso_uneven_counts": (i32, [i32, P64, u64, u64, P64]),
             "rso_uneven_seed": (u64, [u64, u64]),
             "rso_edges": (None, [u64, P64, u64, P64]),
+            "rso_algb": (i32, [u64, u64, u64, dbl, P64, C.c_uint32, C.POINTER(C.c_uint32)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -321,3 +322,12 @@ def gnm(V, m, seed):
 def gnp(V, p, seed):
     return edges(V, bernoulli(V * (V - 1) // 2, p, seed))
 
+
+
+def algb(N, n, seed, slack=4.0, max_attempts=1000):
+    """NEXT-4: Algorithm B + repair (rso_algb): (sorted sample, attempts)."""
+    out = np.zeros(max(int(n), 1), dtype=np.uint64)
+    att = C.c_uint32()
+    _check(lib().rso_algb(int(N), int(n), int(seed) % 2**64, float(slack), _p64(out),
+                          int(max_attempts), C.byref(att)))
+    return out[: int(n)].copy(), att.value

@@ -1035,3 +1035,46 @@ void rso_edges(u64 V, const u64 *values, u64 count, u64 *out)
         out[i] = (lo << 32) | v;
     }
 }
+
+/* NEXT-4: Algorithm B with repair (the paper's GPU variant
+ * P:621-637), the comparison baseline.  Step by step:
+ *   rho' = min(1, (n + slack*sqrt(n)) / N)        ("rho somewhat larger than
+ *          n/N"; reading R14: slack standard deviations)
+ *   for attempt a = 0, 1, ...: seed_a = seed + a*0x9E3779B97F4A7C15 (mod 2^64)
+ *     S = Bernoulli(N, rho', seed_a) (rso_bernoulli), n' = |S|
+ *     if n' >= n stop, else restart ("simply restart")
+ *   R = the WOR sample of n' - n positions from 1..n' with seed_a
+ *       (rso_sample_wor; "Algorithm R to generate n'-n samples from the range
+ *       0..n'-1", P:630-632 -- 1-based here)
+ *   out = S without the elements at positions R ("marks the appropriate
+ *       positions ... for removal ... compacted").
+ * Returns 0, RSO_EINVAL for n > N or a bad slack, -2 past max_attempts. */
+int rso_algb(u64 N, u64 n, u64 seed, double slack, u64 *out, u32 max_attempts, u32 *attempts)
+{
+    if (n > N || !(slack >= 0.0 && slack < 1e300) || N >= ((u64)1 << 63)) return RSO_EINVAL;
+    *attempts = 0;
+    if (n == 0) return RSO_OK;
+    double rho = ((double)n + slack * sqrt((double)n)) / (double)N;
+    if (rho > 1.0) rho = 1.0;
+    for (u32 a = 0; a < max_attempts; a++) {
+        const u64 sa = seed + 0x9E3779B97F4A7C15ull * (u64)a;
+        u64 np = 0;
+        int st = rso_bernoulli(N, rho, sa, NULL, 0, &np);     /* count only */
+        if (st != RSO_OK && st != RSO_ECAPACITY) return st;
+        *attempts = a + 1;
+        if (np < n) continue;
+        u64 *S = (u64 *)malloc((np ? np : 1) * sizeof(u64));
+        u64 *R = (u64 *)malloc((np - n ? np - n : 1) * sizeof(u64));
+        u64 c2 = 0;
+        rso_bernoulli(N, rho, sa, S, np, &c2);
+        st = rso_sample_wor(np, np - n, sa, R, 1);
+        u64 o = 0, t = 0;
+        for (u64 i = 0; i < np; i++) {               /* position i + 1 removed? */
+            if (t < np - n && R[t] == i + 1) { t++; continue; }
+            out[o++] = S[i];
+        }
+        free(S); free(R);
+        return (st == 0 && c2 == np && o == n && t == np - n) ? RSO_OK : RSO_EINVAL;
+    }
+    return -2;
+}

@@ -58,6 +58,8 @@ SIGNATURES = {
     "rs_uneven_seed": (_u64, [_u64, _u64]),
     "rs_gnm": (_int, [_u64, _u64, _u64, _vp, _vp]),
     "rs_gnp": (_int, [_u64, _dbl, _u64, _vp, _u64, _vp, _vp]),
+    "rs_sample_wor_algb": (_int, [_u64, _u64, _u64, _dbl, C.c_uint32, _vp, C.POINTER(C.c_uint32), _vp, _sz, _vp]),
+    "rs_algb_workspace_bytes": (_u64, [_u64, _u64, _dbl]),
     "rs_sample_node": (_int, [_int, _u64, _u64, _u64, _int, _u64, _vp, _vp]),
     "rs_timing_enable": (_int, [_int]),
     "rs_timing_read": (_int, [_int, C.POINTER(_dbl), _P64]),
@@ -320,6 +322,25 @@ def gnp(V: int, p: float, seed: int, capacity=None, out=None, device="cuda", str
     if c > cap:
         raise RSError("gnp: capacity exceeded")
     return o[:c]
+
+
+def algb_workspace_bytes(N: int, n: int, slack: float = 4.0) -> int:
+    return int(lib().rs_algb_workspace_bytes(N, n, float(slack)))
+
+
+def sample_wor_algb(N: int, n: int, seed: int, slack: float = 4.0, max_attempts: int = 1000,
+                    out=None, ws=None, device="cuda", stream=None, return_attempts=False):
+    """NEXT-4: Algorithm B + repair (the paper's B_GPU design, P:191-208,
+    P:621-637) -- a uniform sorted n-subset of 1..N, NOT the same one as
+    sample_wor.  Synchronous (n' goes to the host after each Bernoulli pass).
+    ws: optional uint8 device tensor of algb_workspace_bytes(N, n, slack)."""
+    _require_cuda()
+    o = _out(n, out, device)
+    att = C.c_uint32()
+    _check(lib().rs_sample_wor_algb(N, n, seed % 2**64, float(slack), int(max_attempts), _ptr(o),
+                                    C.byref(att), _ptr(ws) if ws is not None else None,
+                                    ws.numel() if ws is not None else 0, _stream(stream)))
+    return (o[:n], att.value) if return_attempts else o[:n]
 
 
 def unpack_edges(e):

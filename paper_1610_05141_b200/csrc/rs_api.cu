@@ -427,10 +427,14 @@ rs_status bern_call(u64 N, double rho, u64 seed, int world, int rank, u64 *out, 
     Span sp(2, cs);
     {
         const u64 rmax = (N >> p.Db) + ((N & ((1ull << p.Db) - 1)) != 0);   // largest chunk range
-        const bool r16 = rmax <= (1ull << 16);
-        void (*bk)(BernArgs) = gV ? (r16 ? k_bernoulli_g : rmax <= (1ull << 24) ? k_bernoulli32_g : k_bernoulli64_g)
-                                  : (r16 ? k_bernoulli : rmax <= (1ull << 24) ? k_bernoulli32 : k_bernoulli64);
-        const int nt = r16 ? 32 * BNW16 : rmax <= (1ull << 24) ? 64 : 32;
+        const int cls = rmax <= (1ull << 16) ? 0 : rmax <= (1ull << 24) ? 1 : rmax <= (1ull << 32) ? 2 : 3;
+        const bool d = rho < BF64_RHO;
+        void (*const plain[4])(BernArgs) = {k_bernoulli, d ? k_bernoulli32d : k_bernoulli32,
+                                            d ? k_bernoulli64d : k_bernoulli64, k_bernoulli64w};
+        void (*const graph[4])(BernArgs) = {k_bernoulli_g, d ? k_bernoulli32d_g : k_bernoulli32_g,
+                                            d ? k_bernoulli64d_g : k_bernoulli64_g, k_bernoulli64w_g};
+        void (*bk)(BernArgs) = gV ? graph[cls] : plain[cls];
+        const int nt = cls == 0 ? 32 * BNW16 : cls == 3 ? 32 : 32 * RS_B64W;
         int per = 0, dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -442,6 +446,86 @@ rs_status bern_call(u64 N, double rho, u64 seed, int world, int rank, u64 *out, 
     sp.end();
     ++t_launches;
     st = cuda_ok();
+    if (own) cudaFreeAsync(w, cs);
+    return st;
+}
+
+// ---------------------------------------------------------------------------
+// NEXT-4: Algorithm B + repair, composed from the
+// Bernoulli kernel, the WOR sampler (for the positions to remove) and the
+// compaction kernel (rs_algb.cuh).
+// ---------------------------------------------------------------------------
+double algb_rho(u64 N, u64 n, double slack)          // rho' (R14)
+{
+    const double rho = ((double)n + slack * sqrt((double)n)) / (double)N;
+    return rho > 1.0 ? 1.0 : rho;
+}
+
+// workspace: the Bernoulli pass (capacity + count) and the removal positions
+// (at most capacity - n)
+size_t algb_ws_bytes(u64 N, u64 n, double slack, u64 *cap_out)
+{
+    const double rho = algb_rho(N, n, slack);
+    const u64 cap = rs_bernoulli_capacity(N, rho);
+    if (cap_out) *cap_out = cap;
+    BernPlan bp;
+    const size_t bb = plan_bern(N, rho, 1, 0, bp) == RS_OK ? bp.bytes : 0;
+    return align256((cap + 4) * 8) + align256((cap > n ? cap - n : 1) * 8) + align256(bb);
+}
+
+rs_status algb_call(u64 N, u64 n, u64 seed, double slack, u32 max_attempts, u64 *out, u32 *attempts,
+                    void *ws, size_t ws_bytes, void *stream)
+{
+    if (attempts) *attempts = 0;
+    if (n > N || !(slack >= 0.0 && slack < 1e300) || N >= (1ull << 63)) return RS_EINVAL;
+    if (!have_device()) return RS_ECUDA;
+    if (n == 0) return RS_OK;
+    const double rho = algb_rho(N, n, slack);
+    u64 cap = 0;
+    const size_t need = algb_ws_bytes(N, n, slack, &cap);
+    const cudaStream_t cs = S(stream);
+    unsigned char *w = (unsigned char *)ws;
+    const bool own = w == nullptr;
+    if (own) {
+        if (cudaMallocAsync((void **)&w, need, cs) != cudaSuccess) return RS_ENOMEM;
+    } else if (ws_bytes < need) {
+        return RS_ENOMEM;
+    }
+    u64 *tmp = (u64 *)w;
+    u64 *cnt_dev = tmp + cap + 1;
+    u64 *rem = (u64 *)(w + align256((cap + 4) * 8));
+    unsigned char *bws = w + align256((cap + 4) * 8) + align256((cap > n ? cap - n : 1) * 8);
+    const size_t bws_bytes = need - (size_t)(bws - w);
+    rs_status st = RS_EATTEMPTS;
+    for (u32 a = 0; a < max_attempts; ++a) {
+        const u64 sa = seed + 0x9E3779B97F4A7C15ull * (u64)a;
+        st = bern_call(N, rho, sa, 1, 0, tmp, cap, cnt_dev, bws_bytes ? bws : nullptr, bws_bytes, stream);
+        if (st != RS_OK) break;
+        u64 np = 0;                                        // n' to the host
+        if (cudaMemcpyAsync(&np, cnt_dev, 8, cudaMemcpyDeviceToHost, cs) != cudaSuccess ||
+            cudaStreamSynchronize(cs) != cudaSuccess) { st = RS_ECUDA; break; }
+        if (attempts) *attempts = a + 1;
+        if (np > cap) { st = RS_ECAPACITY; break; }
+        if (np < n) { st = RS_EATTEMPTS; continue; }     // restart
+        const u64 r = np - n;
+        if (r == 0) {
+            st = cudaMemcpyAsync(out, tmp, n * 8, cudaMemcpyDeviceToDevice, cs) == cudaSuccess ? RS_OK : RS_ECUDA;
+            break;
+        }
+        st = tree_call(RS_MODE_WOR, np, r, sa, 1, 0, rem, nullptr, 0, stream);   // positions to remove
+        if (st == RS_OK) {
+            Span sp(3, cs);
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const u64 tiles = (np + AB_TILE - 1) / AB_TILE, g = (u64)sms * 8;
+            k_algb_compact<<<(unsigned)(tiles < g ? tiles : g), AB_THREADS, 0, cs>>>(tmp, np, rem, r, out);
+            sp.end();
+            ++t_launches;
+            st = cuda_ok();
+        }
+        break;
+    }
     if (own) cudaFreeAsync(w, cs);
     return st;
 }
@@ -579,6 +663,18 @@ rs_status rs_gnp(uint64_t V, double p, uint64_t seed, uint64_t *edges, uint64_t 
     u64 N;
     if (!edge_count(V, &N)) return ret(RS_EINVAL);
     return ret(bern_call(N, p, seed, 1, 0, edges, capacity, count_dev, nullptr, 0, stream, V));
+}
+
+rs_status rs_sample_wor_algb(uint64_t N, uint64_t n, uint64_t seed, double slack, uint32_t max_attempts,
+                             uint64_t *out, uint32_t *attempts, void *ws, size_t ws_bytes, void *stream)
+{
+    return ret(algb_call(N, n, seed, slack, max_attempts, out, attempts, ws, ws_bytes, stream));
+}
+
+uint64_t rs_algb_workspace_bytes(uint64_t N, uint64_t n, double slack)
+{
+    if (n > N || n == 0 || !(slack >= 0.0 && slack < 1e300)) return 0;
+    return algb_ws_bytes(N, n, slack, nullptr);
 }
 
 rs_status rs_uneven_counts(int p, const uint64_t *L, uint64_t n, uint64_t seed, uint64_t *counts)
@@ -824,6 +920,7 @@ const char *rs_status_string(rs_status s)
     case RS_ECUDA: return "CUDA error or no device";
     case RS_ENOMEM: return "workspace allocation failed or too small";
     case RS_ECAPACITY: return "capacity exceeded";
+    case RS_EATTEMPTS: return "restart budget exhausted (Algorithm B)";
     }
     return "unknown status";
 }

@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep4_wr(LevelArgs a) { s
 #include "rs_leaf.cuh"
 #include "rs_leaf_warp.cuh"
 #include "rs_leaf_bitmap.cuh"
+#include "rs_algb.cuh"
 
 namespace rs {
 
@@ -179,6 +180,62 @@ __device__ __forceinline__ u32 skip_fast(u32 a, u32 b, float c, float m_abs, u32
     return lo >= rf ? r : (u32)fminf(lo, rf);
 }
 
+// fp64 candidate for large mean skips (small rho: there the fp32 margin
+// m_abs = 2^-19 / |lr| fails often).  log_fast is R4's log_ (same reduction,
+// same polynomial, the general-case formula) with the IEEE division
+// f / (2 + f) replaced by an approximate reciprocal and two Newton steps, and
+// no special cases (U = u52 is normal and in (0, 1)): it differs from log_ by
+// a few ulp of |log U| <= 37, i.e. < 2^-44; the margin below allows 2^-42
+// plus 2^-48 relative for the two roundings of q, against CANON's IEEE
+// division by lr.  As with skip_fast, an uncertain floor goes to skip_exact.
+__device__ __forceinline__ double log_fast(double x)
+{
+    const double ln2_hi = 0x1.62e42fee00000p-1, ln2_lo = 0x1.a39ef35793c76p-33;
+    const double L1 = 0x1.5555555555593p-1, L2 = 0x1.999999997fa04p-2,
+                 L3 = 0x1.2492494229359p-2, L4 = 0x1.c71c51d8e78afp-3,
+                 L5 = 0x1.7466496cb03dep-3, L6 = 0x1.39a09d078c69fp-3,
+                 L7 = 0x1.2f112df3e5244p-3;
+    const u64 bits = as_bits(x);
+    const int hi = (int)(bits >> 32);
+    const int mant = hi & 0x000fffff;
+    const int half = (mant + 0x95f64) & 0x100000;
+    const int e = (hi >> 20) - 1023 + (half >> 20);
+    const double xr = from_bits(((u64)(u32)(mant | (half ^ 0x3ff00000)) << 32) | (bits & 0xffffffffull));
+    const double f = xr - 1.0, de = (double)e, d = 2.0 + f;
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    y = fma(y, fma(-d, y, 1.0), y);
+    y = fma(y, fma(-d, y, 1.0), y);
+    const double s = f * y;
+    const double z = s * s;
+    const double w = z * z;
+    const double t1 = w * (L2 + w * (L4 + w * L6));
+    const double t2 = z * (L1 + w * (L3 + w * (L5 + w * L7)));
+    const double R = t2 + t1;
+    return de * ln2_hi - ((s * (f - R) - de * ln2_lo) - f);
+}
+
+__device__ __forceinline__ u32 skip_fast64(u32 a, u32 b, double il, double m_abs, u32 r, bool full, bool &ok)
+{
+    const double q = log_fast(u52(a, b)) * il;                      // ~ log(U) / lr  (>= 0)
+    const double mg = m_abs + q * 0x1p-48;
+    const double lo = floor(q - mg), hi = floor(q + mg);
+    const double rf = (double)r;
+    ok = (lo >= rf && full) || (lo == hi && lo >= 0.0 && lo < rf);
+    return lo >= rf ? r : (u32)fmin(fmax(lo, 0.0), rf);
+}
+
+struct SkipParams {
+    float c, m_abs;          // fp32 path: ln 2 / lr, margin
+    double il, m_abs64;      // fp64 path: 1 / lr, margin
+};
+
+template <bool F64>
+__device__ __forceinline__ u32 skip_cand(u32 a, u32 b, const SkipParams &sp, u32 r, bool full, bool &ok)
+{
+    return F64 ? skip_fast64(a, b, sp.il, sp.m_abs64, r, full, ok) : skip_fast(a, b, sp.c, sp.m_abs, r, full, ok);
+}
+
 __device__ __forceinline__ void st_relaxed(u64 *p, u64 v)
 {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -207,9 +264,9 @@ constexpr int BW_WARPS = 4;
 // ticket before they wait for the previous one's prefix (INC), so neither a
 // slow predecessor nor a long look-back walk stalls them.  T = position
 // arithmetic (u32 while a batch's 64 steps fit, else u64).
-template <typename T, typename B, int G, u32 CAP>
-__device__ __forceinline__ u32 bern_ticket(const BernArgs &a, u64 tk, B *bw, u32 (&cnt)[G], float c,
-                                           float m_abs, u32 lane, bool &overflow)
+template <typename T, typename B, int G, u32 CAP, bool F64>
+__device__ __forceinline__ u32 bern_ticket(const BernArgs &a, u64 tk, B *bw, u32 (&cnt)[G], const SkipParams &sp,
+                                           u32 lane, bool &overflow)
 {
     u32 total = 0;
 #pragma unroll
@@ -234,10 +291,10 @@ __device__ __forceinline__ u32 bern_ticket(const BernArgs &a, u64 tk, B *bw, u32
             const u32x4 w0 = philox_rk(2 * (q0 + lane), st, a.rk);
             const u32x4 w1 = philox_rk(2 * (q0 + lane) + 1, st, a.rk);
             bool ok0, ok1, ok2, ok3;
-            const u32 g0 = skip_fast(w0.x, w0.y, c, m_abs, r32, rfull, ok0);
-            const u32 g1 = skip_fast(w0.z, w0.w, c, m_abs, r32, rfull, ok1);
-            const u32 g2 = skip_fast(w1.x, w1.y, c, m_abs, r32, rfull, ok2);
-            const u32 g3 = skip_fast(w1.z, w1.w, c, m_abs, r32, rfull, ok3);
+            const u32 g0 = skip_cand<F64>(w0.x, w0.y, sp, r32, rfull, ok0);
+            const u32 g1 = skip_cand<F64>(w0.z, w0.w, sp, r32, rfull, ok1);
+            const u32 g2 = skip_cand<F64>(w1.x, w1.y, sp, r32, rfull, ok2);
+            const u32 g3 = skip_cand<F64>(w1.z, w1.w, sp, r32, rfull, ok3);
             T s0 = (T)g0 + 1, s1 = (T)g1 + 1, s2 = (T)g2 + 1, s3 = (T)g3 + 1;
             if (__any_sync(0xffffffffu, !(ok0 && ok1 && ok2 && ok3))) {   // rare: exact fp64 (CANON)
                 if (!ok0) s0 = skip_exact<T>(u52(w0.x, w0.y), a.log1m_rho, r);
@@ -388,15 +445,18 @@ __device__ __forceinline__ u64 bern_wait_inc(const BernArgs &a, u64 tk)
     return v & B_VAL;
 }
 
-template <typename T, typename B, int G, u32 CAP, int NW, bool GR>
+template <typename T, typename B, int G, u32 CAP, int NW, bool GR, bool F64>
 __device__ __forceinline__ void bernoulli_chunks(const BernArgs &a)
 {
     __shared__ B buf[NW][2][CAP];
     const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const u64 ntick = (a.nchunks + G - 1) / G;
     if (blockIdx.x == 0 && wid == 0) { bern_scanner(a, ntick, lane); return; }
-    const float c = (float)(0x1.62e42fefa39efp-1 / a.log1m_rho);   // ln 2 / lr
-    const float m_abs = (float)(0x1p-19 / -a.log1m_rho) + 0x1p-20f;
+    SkipParams sp;
+    sp.c = (float)(0x1.62e42fefa39efp-1 / a.log1m_rho);            // ln 2 / lr
+    sp.m_abs = (float)(0x1p-19 / -a.log1m_rho) + 0x1p-20f;
+    sp.il = 1.0 / a.log1m_rho;
+    sp.m_abs64 = 0x1p-42 / -a.log1m_rho;
     bool overflow = false, have_prev = false;
     u32 cur = 0, prev_cnt[G], prev_total = 0;
     u64 prev_tk = 0;
@@ -406,7 +466,7 @@ __device__ __forceinline__ void bernoulli_chunks(const BernArgs &a)
         tk = __shfl_sync(0xffffffffu, tk, 0);
         if (tk < ntick) {
             u32 cnt[G];
-            bern_ticket<T, B, G, CAP>(a, tk, buf[wid][cur], cnt, c, m_abs, lane, overflow);
+            bern_ticket<T, B, G, CAP, F64>(a, tk, buf[wid][cur], cnt, sp, lane, overflow);
             u32 total = 0;
 #pragma unroll
             for (int g = 0; g < G; ++g) total += cnt[g];
@@ -438,17 +498,37 @@ __device__ __forceinline__ void bernoulli_chunks(const BernArgs &a)
 #ifndef RS_BG
 #define RS_BG 2
 #endif
+#ifndef RS_B64W
+#define RS_B64W 4
+#endif
 constexpr int BG16 = RS_BG;                                           // chunks per ticket (u16 path)
 constexpr u32 BCAP16 = ((BG16 * 1024 + 10 * 32 * (BG16 < 4 ? 2 : BG16 / 2) + 63) / 64) * 64;
 constexpr int BNW16 = (BCAP16 * 2 * 2 * 4 <= 48 * 1024) ? 4 : (BCAP16 * 2 * 2 * 2 <= 48 * 1024) ? 2 : 1;
-__global__ void __launch_bounds__(32 * BNW16) k_bernoulli(BernArgs a) { bernoulli_chunks<u32, uint16_t, BG16, BCAP16, BNW16, false>(a); }
-__global__ void __launch_bounds__(32 * BNW16) k_bernoulli_g(BernArgs a) { bernoulli_chunks<u32, uint16_t, BG16, BCAP16, BNW16, true>(a); }
-// r <= 2^24: u32 positions, 2 chunks per ticket (2560 x 4 B per warp)
-__global__ void __launch_bounds__(64) k_bernoulli32(BernArgs a) { bernoulli_chunks<u32, u32, 2, 2560, 2, false>(a); }
-__global__ void __launch_bounds__(64) k_bernoulli32_g(BernArgs a) { bernoulli_chunks<u32, u32, 2, 2560, 2, true>(a); }
-// larger r: u64 positions, 1 chunk per ticket (1536 x 8 B per warp)
-__global__ void __launch_bounds__(32) k_bernoulli64(BernArgs a) { bernoulli_chunks<u64, u64, 1, 1536, 1, false>(a); }
-__global__ void __launch_bounds__(32) k_bernoulli64_g(BernArgs a) { bernoulli_chunks<u64, u64, 1, 1536, 1, true>(a); }
+__global__ void __launch_bounds__(32 * BNW16) k_bernoulli(BernArgs a) { bernoulli_chunks<u32, uint16_t, BG16, BCAP16, BNW16, false, false>(a); }
+__global__ void __launch_bounds__(32 * BNW16) k_bernoulli_g(BernArgs a) { bernoulli_chunks<u32, uint16_t, BG16, BCAP16, BNW16, true, false>(a); }
+// r <= 2^24: u32 positions; 2^24 < r <= 2^32: u64 position arithmetic, u32
+// positions buffered; RS_B32G chunks per ticket.  These chunk ranges mean
+// rho < 2^-6; the "d" kernels take fp64 skip candidates (chosen for
+// rho < BF64_RHO, where the fp32 margin fails too often -- measured
+// crossover)
+#ifndef RS_B32G
+#define RS_B32G 1
+#endif
+constexpr u32 BCAP32 = RS_B32G * 1024 + 512;
+#define RS_BK(name, T, GR, F64) \
+    __global__ void __launch_bounds__(32 * RS_B64W) name(BernArgs a) { bernoulli_chunks<T, u32, RS_B32G, BCAP32, RS_B64W, GR, F64>(a); }
+RS_BK(k_bernoulli32, u32, false, false)
+RS_BK(k_bernoulli32_g, u32, true, false)
+RS_BK(k_bernoulli32d, u32, false, true)
+RS_BK(k_bernoulli32d_g, u32, true, true)
+RS_BK(k_bernoulli64, u64, false, false)
+RS_BK(k_bernoulli64_g, u64, true, false)
+RS_BK(k_bernoulli64d, u64, false, true)
+RS_BK(k_bernoulli64d_g, u64, true, true)
+#undef RS_BK
+// larger r: u64 positions (1536 x 8 B per warp)
+__global__ void __launch_bounds__(32) k_bernoulli64w(BernArgs a) { bernoulli_chunks<u64, u64, 1, 1536, 1, false, true>(a); }
+__global__ void __launch_bounds__(32) k_bernoulli64w_g(BernArgs a) { bernoulli_chunks<u64, u64, 1, 1536, 1, true, true>(a); }
 
 // ===========================================================================
 // Validation helpers.

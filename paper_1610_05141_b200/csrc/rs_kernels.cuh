@@ -178,10 +178,24 @@ struct BernArgs {
 
 __global__ void k_bernoulli(BernArgs a);                           // chunk ranges <= 2^16
 __global__ void k_bernoulli32(BernArgs a);                         // chunk ranges <= 2^24
-__global__ void k_bernoulli64(BernArgs a);                         // larger chunk ranges
+__global__ void k_bernoulli64(BernArgs a);                         // chunk ranges <= 2^32
+__global__ void k_bernoulli64w(BernArgs a);                        // larger chunk ranges
+__global__ void k_bernoulli32d(BernArgs a);                        // fp64 skip candidates (small rho)
+__global__ void k_bernoulli64d(BernArgs a);
+__global__ void k_bernoulli32d_g(BernArgs a);
+__global__ void k_bernoulli64d_g(BernArgs a);
+constexpr double BF64_RHO = 0x1p-12;                               // fp64 candidates below this rho
 __global__ void k_bernoulli_g(BernArgs a);                         // G(n, p) variants (NEXT-3)
 __global__ void k_bernoulli32_g(BernArgs a);
 __global__ void k_bernoulli64_g(BernArgs a);
+__global__ void k_bernoulli64w_g(BernArgs a);
+
+// NEXT-4 (rs_algb.cuh): Algorithm B's repair -- S[0..np) minus the elements at
+// the sorted 1-based positions R[0..nr) -> out (compaction)
+constexpr u32 AB_THREADS = 256, AB_PER = 16, AB_TILE = AB_THREADS * AB_PER, AB_SMAX = 256;
+__global__ void __launch_bounds__(AB_THREADS) k_algb_compact(const u64 *__restrict__ S, u64 np,
+                                                             const u64 *__restrict__ R, u64 nr,
+                                                             u64 *__restrict__ out);
 
 // Validation (tests / bench correctness checks).
 __global__ void k_digest(const u64 *v, u64 n, u64 base, u64 *acc);

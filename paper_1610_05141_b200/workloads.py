@@ -22,6 +22,9 @@ CFG4 = dict(name="cfg4_wr_n2^32_N2^36", mode="wr", N=2 ** 36, n=2 ** 32, seed=1)
 # NEXT-3: G(V, m) with the edge decode fused into the leaf stores
 GNM = dict(name="gnm_V2^23_m2^32", mode="gnm", V=2 ** 23, N=2 ** 22 * (2 ** 23 - 1), n=2 ** 32, seed=1)
 
+# NEXT-4: Algorithm B + repair on the headline shape
+ALGB = dict(name="algb_wor_n2^32_N2^48", mode="algb", N=2 ** 48, n=2 ** 32, seed=1, slack=4.0)
+
 ALL = [CFG0, CFG1, HEADLINE, CFG3A, CFG3B, CFG3B_ROOF, CFG4]
 PARITY_SEEDS = [0, 1, 0xDEADBEEF, 2 ** 64 - 1]
 

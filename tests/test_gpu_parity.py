@@ -105,7 +105,10 @@ def test_wr_full_compare(N, n):
 # chunk ranges r <= 2^16 (u16 buffers, 4 chunks per ticket), <= 2^24 (u32), above (u64)
 BERN_CASES = [(2 ** 24, 0.01), (10 ** 6 + 17, 0.3), (2 ** 20, 1e-3), (1000, 0.999), (5, 0.5),
               (2 ** 26, 1e-5), (1000, 0.0), (1000, 1.0), (0, 0.5), (2 ** 30, 1e-6),
-              (2 ** 40 + 3, 1e-9), (3 * 10 ** 8, 0.5)]
+              (2 ** 40 + 3, 1e-9), (3 * 10 ** 8, 0.5),
+              # fp64 skip candidates: u32 chunks (r <= 2^24), u64 arithmetic with
+              # u32 positions (r <= 2^32), u64 positions (r > 2^32)
+              (2 ** 32, 1e-4), (2 ** 37 + 5, 2 ** -16), (2 ** 50, 1e-9)]
 
 
 @pytest.mark.parametrize("N,rho", BERN_CASES)
@@ -303,3 +306,48 @@ def test_gnm_cta_path():
 def test_gnp(V, p):
     got = _np(rs.gnp(V, p, 17))
     assert np.array_equal(got, O.gnp(V, p, 17)), (V, p)
+
+
+# ---- NEXT-4: Algorithm B + repair (the comparison baseline) -----------------
+
+ALGB_CASES = [(1, 1, 4.0), (10, 10, 4.0), (100, 95, 4.0), (1000, 100, 0.0), (2 ** 20, 2 ** 10, 4.0),
+              (2 ** 30, 2 ** 20, 4.0), (2 ** 40, 3 * 10 ** 6, 2.0), (2 ** 48, 5000, 0.5)]
+
+
+@pytest.mark.parametrize("N,n,slack", ALGB_CASES)
+def test_algb(N, n, slack):
+    for seed in (3, 2 ** 64 - 1):
+        got, att = rs.sample_wor_algb(N, n, seed, slack=slack, return_attempts=True)
+        exp, eatt = O.algb(N, n, seed, slack=slack)
+        assert att == eatt, (N, n, seed)
+        assert np.array_equal(_np(got), exp), (N, n, seed)
+    _no_device_errors()
+
+
+def test_algb_restarts_and_errors():
+    # slack 0 restarts about half the time: the attempt counts and outputs
+    # follow the oracle's seed_a sequence
+    for seed in range(12):
+        got, att = rs.sample_wor_algb(1000, 100, seed, slack=0.0, return_attempts=True)
+        exp, eatt = O.algb(1000, 100, seed, slack=0.0)
+        assert att == eatt and np.array_equal(_np(got), exp)
+    assert rs.sample_wor_algb(50, 0, 1).numel() == 0
+    N, n = 2 ** 30, 2 ** 16                      # caller workspace, and one too small
+    ws = torch.empty(rs.algb_workspace_bytes(N, n), dtype=torch.uint8, device="cuda")
+    got, att = rs.sample_wor_algb(N, n, 9, ws=ws, return_attempts=True)
+    exp, eatt = O.algb(N, n, 9)
+    assert att == eatt and np.array_equal(_np(got), exp)
+    with pytest.raises(rs.RSError):
+        rs.sample_wor_algb(N, n, 9, ws=ws[:1024])
+    with pytest.raises(rs.RSError):
+        rs.sample_wor_algb(10, 11, 1)
+    with pytest.raises(rs.RSError):
+        rs.sample_wor_algb(10, 5, 1, slack=-1.0)
+    fails = 0
+    for seed in range(40):          # one pass only: fails whenever n' < n
+        try:
+            rs.sample_wor_algb(1000, 100, seed, slack=0.0, max_attempts=1)
+        except rs.RSError as e:
+            assert "restart" in str(e)
+            fails += 1
+    assert 5 < fails < 35
