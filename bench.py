@@ -284,7 +284,7 @@ def run_native(args):
 
         def step():
             if mode == "gnm":
-                rs.gnm(wl["V"], n, seed, out=out)
+                rs.gnm(wl["V"], n, seed, out=out, ws=ws)
             else:
                 fn(N, n, seed, world, rank, out, ws)
             if world > 1:

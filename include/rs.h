@@ -120,10 +120,13 @@ rs_status rs_sample_node(int mode, uint64_t N, uint64_t n, uint64_t seed, int de
  * -> RS_EINVAL).  rs_gnp: each edge independently with probability p;
  * capacity / count_dev as rs_bernoulli (capacity from
  * rs_bernoulli_capacity(V(V-1)/2, p)).  Outputs equal the decoded
- * rs_sample_wor / rs_bernoulli samples over 1..V(V-1)/2 with the same seed. */
-rs_status rs_gnm(uint64_t V, uint64_t m, uint64_t seed, uint64_t *edges, void *stream);
+ * rs_sample_wor / rs_bernoulli samples over 1..V(V-1)/2 with the same seed.
+ * ws: NULL (cudaMallocAsync on the stream) or a device workspace of ws_bytes
+ * >= rs_workspace_bytes(RS_MODE_WOR / RS_MODE_BERNOULLI, V(V-1)/2, m, p, 1). */
+rs_status rs_gnm(uint64_t V, uint64_t m, uint64_t seed, uint64_t *edges, void *ws, size_t ws_bytes,
+                 void *stream);
 rs_status rs_gnp(uint64_t V, double p, uint64_t seed, uint64_t *edges, uint64_t capacity,
-                 uint64_t *count_dev, void *stream);
+                 uint64_t *count_dev, void *ws, size_t ws_bytes, void *stream);
 
 /* ---- Algorithm B + repair (NEXT-4, the comparison baseline) -------------
  * The paper's own GPU design B_GPU, composed from the

@@ -56,8 +56,8 @@ SIGNATURES = {
     "rs_node_info": (_int, [_int, _u64, _u64, _u64, _int, _u64, _P64, _P64]),
     "rs_uneven_counts": (_int, [_int, _P64, _u64, _u64, _P64]),
     "rs_uneven_seed": (_u64, [_u64, _u64]),
-    "rs_gnm": (_int, [_u64, _u64, _u64, _vp, _vp]),
-    "rs_gnp": (_int, [_u64, _dbl, _u64, _vp, _u64, _vp, _vp]),
+    "rs_gnm": (_int, [_u64, _u64, _u64, _vp, _vp, _sz, _vp]),
+    "rs_gnp": (_int, [_u64, _dbl, _u64, _vp, _u64, _vp, _vp, _sz, _vp]),
     "rs_sample_wor_algb": (_int, [_u64, _u64, _u64, _dbl, C.c_uint32, _vp, C.POINTER(C.c_uint32), _vp, _sz, _vp]),
     "rs_algb_workspace_bytes": (_u64, [_u64, _u64, _dbl]),
     "rs_sample_node": (_int, [_int, _u64, _u64, _u64, _int, _u64, _vp, _vp]),
@@ -302,22 +302,24 @@ def sample_node(mode: int, N: int, n: int, seed: int, depth: int, index: int, ou
     return o[:cnt]
 
 
-def gnm(V: int, m: int, seed: int, out=None, device="cuda", stream=None):
+def gnm(V: int, m: int, seed: int, out=None, ws=None, device="cuda", stream=None):
     """G(V, m): m distinct edges as packed (u << 32) | v, lexicographic order."""
     _require_cuda()
     o = _out(m, out, device)
-    _check(lib().rs_gnm(V, m, seed % 2**64, _ptr(o), _stream(stream)))
+    _check(lib().rs_gnm(V, m, seed % 2**64, _ptr(o), _ptr(ws) if ws is not None else None,
+                        ws.numel() if ws is not None else 0, _stream(stream)))
     return o[:m]
 
 
-def gnp(V: int, p: float, seed: int, capacity=None, out=None, device="cuda", stream=None):
+def gnp(V: int, p: float, seed: int, capacity=None, out=None, ws=None, device="cuda", stream=None):
     """G(V, p): every edge with probability p, packed (u << 32) | v, sorted."""
     _require_cuda()
     N = V * (V - 1) // 2
     cap = bernoulli_capacity(N, p) if capacity is None else capacity
     o = _out(cap, out, device)
     cnt = torch.zeros(1, dtype=torch.uint64, device=o.device)
-    _check(lib().rs_gnp(V, float(p), seed % 2**64, _ptr(o), cap, _ptr(cnt), _stream(stream)))
+    _check(lib().rs_gnp(V, float(p), seed % 2**64, _ptr(o), cap, _ptr(cnt), _ptr(ws) if ws is not None else None,
+                        ws.numel() if ws is not None else 0, _stream(stream)))
     c = int(cnt.item())
     if c > cap:
         raise RSError("gnp: capacity exceeded")

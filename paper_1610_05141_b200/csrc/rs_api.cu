@@ -645,7 +645,8 @@ static bool edge_count(uint64_t V, uint64_t *N)
     return true;
 }
 
-rs_status rs_gnm(uint64_t V, uint64_t m, uint64_t seed, uint64_t *edges, void *stream)
+rs_status rs_gnm(uint64_t V, uint64_t m, uint64_t seed, uint64_t *edges, void *ws, size_t ws_bytes,
+                 void *stream)
 {
     u64 N;
     if (!edge_count(V, &N)) return ret(RS_EINVAL);
@@ -654,15 +655,15 @@ rs_status rs_gnm(uint64_t V, uint64_t m, uint64_t seed, uint64_t *edges, void *s
     rs_status st = plan_tree(RS_MODE_WOR, N, m, seed, 1, 0, p);
     if (st != RS_OK) return ret(st);
     p.gV = V;
-    return ret(plan_call(p, edges, nullptr, 0, stream));
+    return ret(plan_call(p, edges, ws, ws_bytes, stream));
 }
 
 rs_status rs_gnp(uint64_t V, double p, uint64_t seed, uint64_t *edges, uint64_t capacity,
-                 uint64_t *count_dev, void *stream)
+                 uint64_t *count_dev, void *ws, size_t ws_bytes, void *stream)
 {
     u64 N;
     if (!edge_count(V, &N)) return ret(RS_EINVAL);
-    return ret(bern_call(N, p, seed, 1, 0, edges, capacity, count_dev, nullptr, 0, stream, V));
+    return ret(bern_call(N, p, seed, 1, 0, edges, capacity, count_dev, ws, ws_bytes, stream, V));
 }
 
 rs_status rs_sample_wor_algb(uint64_t N, uint64_t n, uint64_t seed, double slack, uint32_t max_attempts,

@@ -344,8 +344,9 @@ __device__ __forceinline__ u32 bern_ticket(const BernArgs &a, u64 tk, B *bw, u32
 template <typename B>
 __device__ __noinline__ void bern_store_edges(u64 *d, const B *bw, u32 lim, u64 base, u64 gV, u32 lane)
 {
+    EdgeCursor cur(gV);
 #pragma unroll 1
-    for (u32 i = lane; i < lim; i += 32) d[i] = edge_pack(gV, base - 1 + (u64)bw[i]);
+    for (u32 i = lane; i < lim; i += 32) d[i] = cur.pack(base - 1 + (u64)bw[i]);
 }
 
 template <typename B, int G, bool GR>

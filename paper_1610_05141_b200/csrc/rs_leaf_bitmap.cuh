@@ -61,6 +61,8 @@ __device__ __forceinline__ void bitmap_leaves(const LeafArgs &a)
         if (nout == 0) continue;
         u64 *dst = COMP ? a.out + (g.lo - a.out_base - a.off[L]) : a.out + a.off[L];
         const u64 base = g.lo + 1;
+        EdgeCursor ecur(a.gV);                      // graph calls: per-lane values ascend
+        auto ow = [&](u64 x) -> u64 { return GR ? ecur.pack(x - 1) : x; };
         for (u32 w = lane; w < nw; w += 32) sh.bm[w] = 0u;
         __syncwarp();
         if (k > 0) {
@@ -94,16 +96,16 @@ __device__ __forceinline__ void bitmap_leaves(const LeafArgs &a)
                 const u32 b2 = COMP ? ~W4.z : W4.z, b3 = COMP ? ~W4.w : W4.w;
                 const u32 p0 = pos, p1 = p0 + __popc(b0), p2 = p1 + __popc(b1), p3 = p2 + __popc(b2);
                 pos = p3 + __popc(b3);
-                if ((b0 >> lane) & 1u) dst[p0 + __popc(b0 & lm)] = out_word_t<GR>(vb, a.gV);
-                if ((b1 >> lane) & 1u) dst[p1 + __popc(b1 & lm)] = out_word_t<GR>(vb + 32, a.gV);
-                if ((b2 >> lane) & 1u) dst[p2 + __popc(b2 & lm)] = out_word_t<GR>(vb + 64, a.gV);
-                if ((b3 >> lane) & 1u) dst[p3 + __popc(b3 & lm)] = out_word_t<GR>(vb + 96, a.gV);
+                if ((b0 >> lane) & 1u) dst[p0 + __popc(b0 & lm)] = ow(vb);
+                if ((b1 >> lane) & 1u) dst[p1 + __popc(b1 & lm)] = ow(vb + 32);
+                if ((b2 >> lane) & 1u) dst[p2 + __popc(b2 & lm)] = ow(vb + 64);
+                if ((b3 >> lane) & 1u) dst[p3 + __popc(b3 & lm)] = ow(vb + 96);
             }
 #pragma unroll 1
             for (; w < nw; ++w, vb += 32) {
                 const u32 word = sh.bm[w];
                 const u32 bits = COMP ? (~word & bm_valid(w, r)) : word;
-                if ((bits >> lane) & 1u) dst[pos + __popc(bits & lm)] = out_word_t<GR>(vb, a.gV);
+                if ((bits >> lane) & 1u) dst[pos + __popc(bits & lm)] = ow(vb);
                 pos += __popc(bits);
             }
         } else {
@@ -122,7 +124,7 @@ __device__ __forceinline__ void bitmap_leaves(const LeafArgs &a)
                 while (bits) {
                     const u32 b = __ffs(bits) - 1;
                     bits &= bits - 1;
-                    dst[pos++] = out_word_t<GR>(base + 32u * w + b, a.gV);
+                    dst[pos++] = ow(base + 32u * w + b);
                 }
             }
         }

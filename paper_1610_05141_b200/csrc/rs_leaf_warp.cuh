@@ -297,8 +297,9 @@ __device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const RoundKeys &K, con
 // non-unrolled loop so the kernel holds a single copy of the decode.
 __device__ __noinline__ void wl_store_edges(const WarpLeaf &sh, u64 *d0, u32 h, u32 k, u64 base, u64 gV, u32 lane)
 {
+    EdgeCursor cur(gV);
 #pragma unroll 1
-    for (u32 i = h + lane; i < h + k; i += 32) d0[i] = edge_pack(gV, base - 1 + sh.keys[i]);
+    for (u32 i = h + lane; i < h + k; i += 32) d0[i] = cur.pack(base - 1 + sh.keys[i]);
     __syncwarp();
 }
 

@@ -351,3 +351,14 @@ def test_algb_restarts_and_errors():
             assert "restart" in str(e)
             fails += 1
     assert 5 < fails < 35
+
+
+def test_graphs_with_workspace():
+    V, m, p = 5000, 10 ** 6, 0.05
+    N = V * (V - 1) // 2
+    ws = torch.empty(rs.workspace_bytes(rs.MODE_WOR, N, m, 0.0, 1), dtype=torch.uint8, device="cuda")
+    assert np.array_equal(_np(rs.gnm(V, m, 4, ws=ws)), O.gnm(V, m, 4))
+    ws = torch.empty(rs.workspace_bytes(rs.MODE_BERNOULLI, N, 0, p, 1), dtype=torch.uint8, device="cuda")
+    assert np.array_equal(_np(rs.gnp(V, p, 4, ws=ws)), O.gnp(V, p, 4))
+    with pytest.raises(rs.RSError):
+        rs.gnm(V, m, 4, ws=ws[:16])
