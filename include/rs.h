@@ -190,9 +190,13 @@ rs_status rs_sample_wor_host(uint64_t N, uint64_t n, uint64_t seed, uint64_t *ou
  * (rs_sample_node; batches of <= 2^27 values) into two device staging
  * buffers, copying batch i to the host on an internal stream while batch
  * i+1 is generated on `stream`.  Synchronous (returns after the last copy).
- * out_host should be pinned for full copy bandwidth. */
+ * out_host should be pinned for full copy bandwidth.  The two staging
+ * buffers (<= 1 GiB each), the tree workspace and the copy stream are kept
+ * per device across calls (calls on one device are serialised by a lock);
+ * rs_release_cache frees them. */
 rs_status rs_sample_shard_host(int mode, uint64_t N, uint64_t n, uint64_t seed, int world,
                                int rank, uint64_t *out_host, void *stream);
+rs_status rs_release_cache(void);
 
 /* ---- validation helpers (tests / benchmarks; not on the hot path) ------
  * rs_digest: *result_dev += sum_i mix64((base_index + i) ^ mix64(v[i]))

@@ -62,6 +62,7 @@ SIGNATURES = {
     "rs_algb_workspace_bytes": (_u64, [_u64, _u64, _dbl]),
     "rs_sample_node": (_int, [_int, _u64, _u64, _u64, _int, _u64, _vp, _vp]),
     "rs_timing_enable": (_int, [_int]),
+    "rs_release_cache": (_int, []),
     "rs_timing_read": (_int, [_int, C.POINTER(_dbl), _P64]),
     "rs_status_string": (C.c_char_p, [_int]),
     "rs_last_status": (_int, []),
@@ -252,6 +253,11 @@ def sample_shard_host(mode: int, N: int, n: int, seed: int, world: int, rank: in
     _check(lib().rs_sample_shard_host(mode, N, n, seed % 2**64, world, rank, _ptr(out_host),
                                       _stream(stream)))
     return out_host[:cnt]
+
+
+def release_cache():
+    """Free the host-buffer calls' cached device staging (rs_release_cache)."""
+    _check(lib().rs_release_cache())
 
 
 # ---- validation helpers ---------------------------------------------------

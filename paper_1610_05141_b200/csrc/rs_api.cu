@@ -530,6 +530,29 @@ rs_status algb_call(u64 N, u64 n, u64 seed, double slack, u32 max_attempts, u64 
     return st;
 }
 
+// Staging for the host-buffer calls, cached per device across calls (a
+// fresh cudaMallocAsync of ~2 GiB per call cost ~250 ms of page mapping,
+// more than the copies of a 2^28-value sample).  One call at a time per
+// device holds it; rs_release_cache() frees it.
+struct HostStage {
+    std::mutex mu;
+    u64 *buf[2] = {nullptr, nullptr};
+    size_t buf_bytes = 0;
+    unsigned char *ws = nullptr;
+    size_t ws_bytes = 0;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t gen_done[2]{}, copy_done[2]{};
+    void release()
+    {
+        if (buf[0]) cudaFree(buf[0]);
+        if (buf[1]) cudaFree(buf[1]);
+        if (ws) cudaFree(ws);
+        buf[0] = buf[1] = nullptr; ws = nullptr; buf_bytes = ws_bytes = 0;
+    }
+};
+constexpr int RS_MAX_DEV = 64;
+HostStage g_stage[RS_MAX_DEV];
+
 }  // namespace
 
 // ===========================================================================
@@ -765,43 +788,68 @@ rs_status rs_sample_shard_host(int mode, uint64_t N, uint64_t n, uint64_t seed, 
         if (plans[i].local_count > maxc) maxc = plans[i].local_count;
         if (plans[i].bytes > maxws) maxws = plans[i].bytes;
     }
-    const cudaStream_t gs = S(stream);
-    cudaStream_t cs;
-    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return ret(RS_ECUDA);
-    cudaEvent_t gen_done[2], copy_done[2];
-    for (int i = 0; i < 2; ++i) {
-        cudaEventCreateWithFlags(&gen_done[i], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&copy_done[i], cudaEventDisableTiming);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= RS_MAX_DEV) return ret(RS_ECUDA);
+    HostStage &H = g_stage[dev];
+    std::lock_guard<std::mutex> lock(H.mu);
+    if (!H.cs) {
+        if (cudaStreamCreateWithFlags(&H.cs, cudaStreamNonBlocking) != cudaSuccess) { H.cs = nullptr; return ret(RS_ECUDA); }
+        for (int i = 0; i < 2; ++i) {
+            cudaEventCreateWithFlags(&H.gen_done[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&H.copy_done[i], cudaEventDisableTiming);
+        }
     }
-    u64 *buf[2] = {nullptr, nullptr};
-    unsigned char *ws = nullptr;
-    st = RS_OK;
-    if (cudaMallocAsync((void **)&buf[0], maxc * 8 + 8, gs) != cudaSuccess ||
-        cudaMallocAsync((void **)&buf[1], maxc * 8 + 8, gs) != cudaSuccess ||
-        cudaMallocAsync((void **)&ws, maxws, gs) != cudaSuccess)
-        st = RS_ENOMEM;
+    const size_t need_buf = align256(maxc * 8 + 8), need_ws = align256(maxws ? maxws : 1);
+    if (H.buf_bytes < need_buf) {
+        if (H.buf[0]) cudaFree(H.buf[0]);
+        if (H.buf[1]) cudaFree(H.buf[1]);
+        H.buf[0] = H.buf[1] = nullptr; H.buf_bytes = 0;
+        if (cudaMalloc((void **)&H.buf[0], need_buf) != cudaSuccess ||
+            cudaMalloc((void **)&H.buf[1], need_buf) != cudaSuccess) { H.release(); cudaGetLastError(); return ret(RS_ENOMEM); }
+        H.buf_bytes = need_buf;
+    }
+    if (H.ws_bytes < need_ws) {
+        if (H.ws) cudaFree(H.ws);
+        H.ws = nullptr; H.ws_bytes = 0;
+        if (cudaMalloc((void **)&H.ws, need_ws) != cudaSuccess) { H.release(); cudaGetLastError(); return ret(RS_ENOMEM); }
+        H.ws_bytes = need_ws;
+    }
+    const cudaStream_t gs = S(stream), cs = H.cs;
+    cudaEventRecord(H.copy_done[0], cs);          // the staging buffers are free once earlier copies end
+    cudaEventRecord(H.copy_done[1], cs);
+    cudaStreamWaitEvent(gs, H.copy_done[0], 0);
     const u64 base_off = sp.global_offset;
     for (u64 i = 0; i < nb && st == RS_OK; ++i) {
         const int j = (int)(i & 1);
-        if (i >= 2) cudaStreamWaitEvent(gs, copy_done[j], 0);       // buffer j is free again
-        st = run_tree(plans[i], buf[j], ws, gs);
-        cudaEventRecord(gen_done[j], gs);
-        cudaStreamWaitEvent(cs, gen_done[j], 0);
+        if (i >= 2) cudaStreamWaitEvent(gs, H.copy_done[j], 0);     // buffer j is free again
+        st = run_tree(plans[i], H.buf[j], H.ws, gs);
+        cudaEventRecord(H.gen_done[j], gs);
+        cudaStreamWaitEvent(cs, H.gen_done[j], 0);
         if (plans[i].local_count &&
-            cudaMemcpyAsync(out_host + (plans[i].global_offset - base_off), buf[j],
+            cudaMemcpyAsync(out_host + (plans[i].global_offset - base_off), H.buf[j],
                             plans[i].local_count * 8, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
             st = RS_ECUDA;
-        cudaEventRecord(copy_done[j], cs);
+        cudaEventRecord(H.copy_done[j], cs);
     }
-    cudaStreamWaitEvent(gs, copy_done[0], 0);
-    cudaStreamWaitEvent(gs, copy_done[1], 0);
-    if (buf[0]) cudaFreeAsync(buf[0], gs);
-    if (buf[1]) cudaFreeAsync(buf[1], gs);
-    if (ws) cudaFreeAsync(ws, gs);
+    cudaStreamWaitEvent(gs, H.copy_done[0], 0);
+    cudaStreamWaitEvent(gs, H.copy_done[1], 0);
     if (cudaStreamSynchronize(gs) != cudaSuccess || cudaStreamSynchronize(cs) != cudaSuccess) st = RS_ECUDA;
-    for (int i = 0; i < 2; ++i) { cudaEventDestroy(gen_done[i]); cudaEventDestroy(copy_done[i]); }
-    cudaStreamDestroy(cs);
     return ret(st);
+}
+
+rs_status rs_release_cache(void)
+{
+    for (int d = 0; d < RS_MAX_DEV; ++d) {
+        std::lock_guard<std::mutex> lock(g_stage[d].mu);
+        if (g_stage[d].buf_bytes || g_stage[d].ws_bytes) {
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(d);
+            g_stage[d].release();
+            cudaSetDevice(cur);
+        }
+    }
+    return ret(RS_OK);
 }
 
 rs_status rs_sample_wor_host(uint64_t N, uint64_t n, uint64_t seed, uint64_t *out_host,

@@ -267,6 +267,13 @@ def test_host_buffer_batched_overlap():
     d = rs.sample_wor(N, n, 5)
     assert torch.equal(h.view(torch.int64), d.cpu().view(torch.int64))
     _sampled_leaf_parity(d, N, n, 5, O.MODE_WOR, nsample=16)
+    # the cached staging: a smaller call reuses it, a WR shard after a release
+    # re-creates it
+    assert np.array_equal(rs.sample_wor_host(2 ** 30, 2 ** 20, 1).numpy(), O.sample_wor(2 ** 30, 2 ** 20, 1))
+    rs.release_cache()
+    hw = rs.sample_shard_host(rs.MODE_WR, 2 ** 36, 2 ** 27, 3, 2, 1)
+    dw = rs.sample_wr_shard(2 ** 36, 2 ** 27, 3, 2, 1)
+    assert torch.equal(hw.view(torch.int64), dw.cpu().view(torch.int64))
 
 
 # ---- NEXT-2: uneven universe over PEs ---------------------------------
