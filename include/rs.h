@@ -198,6 +198,14 @@ rs_status rs_sample_shard_host(int mode, uint64_t N, uint64_t n, uint64_t seed, 
                                int rank, uint64_t *out_host, void *stream);
 rs_status rs_release_cache(void);
 
+/* ---- split deviates (diagnostics / tests) ----------------------------------
+ * out[t] = the split tree's deviate for node id id0 + t (the device code the
+ * split kernels run): kind 0 = hypergeometric X ~ Hyp(k draws, L of R)
+ * (R6), kind 1 = binomial X ~ Bin(k, L/R) (R9).
+ * out: device, count values.  L > R, (kind 0) k > R, R >= 2^63 -> RS_EINVAL. */
+rs_status rs_deviates(int kind, uint64_t k, uint64_t L, uint64_t R, uint64_t seed, uint64_t id0,
+                      uint64_t count, uint64_t *out, void *stream);
+
 /* ---- validation helpers (tests / benchmarks; not on the hot path) ------
  * rs_digest: *result_dev += sum_i mix64((base_index + i) ^ mix64(v[i]))
  * (mod 2^64; order-sensitive, shard-composable; caller zeroes result_dev).

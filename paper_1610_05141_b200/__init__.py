@@ -63,6 +63,7 @@ SIGNATURES = {
     "rs_sample_node": (_int, [_int, _u64, _u64, _u64, _int, _u64, _vp, _vp]),
     "rs_timing_enable": (_int, [_int]),
     "rs_release_cache": (_int, []),
+    "rs_deviates": (_int, [_int, _u64, _u64, _u64, _u64, _u64, _u64, _vp, _vp]),
     "rs_timing_read": (_int, [_int, C.POINTER(_dbl), _P64]),
     "rs_status_string": (C.c_char_p, [_int]),
     "rs_last_status": (_int, []),
@@ -253,6 +254,14 @@ def sample_shard_host(mode: int, N: int, n: int, seed: int, world: int, rank: in
     _check(lib().rs_sample_shard_host(mode, N, n, seed % 2**64, world, rank, _ptr(out_host),
                                       _stream(stream)))
     return out_host[:cnt]
+
+
+def deviates(kind: int, k: int, L: int, R: int, seed: int, id0: int, count: int, stream=None):
+    """The split tree's deviates for node ids id0..id0+count-1 (0 = HGD, 1 = BIN)."""
+    _require_cuda()
+    o = torch.empty(count, dtype=torch.uint64, device="cuda")
+    _check(lib().rs_deviates(kind, k, L, R, seed % 2**64, id0, count, _ptr(o), _stream(stream)))
+    return o
 
 
 def release_cache():

@@ -553,6 +553,12 @@ struct HostStage {
 constexpr int RS_MAX_DEV = 64;
 HostStage g_stage[RS_MAX_DEV];
 
+__global__ void k_deviates(int kind, u64 k, u64 L, u64 R, u64 seed, u64 id0, u64 count, u64 *out)
+{
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count; i += (u64)gridDim.x * blockDim.x)
+        out[i] = kind ? binom(k, L, R, seed, id0 + i) : hgd(k, L, R, seed, id0 + i);
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -835,6 +841,19 @@ rs_status rs_sample_shard_host(int mode, uint64_t N, uint64_t n, uint64_t seed, 
     cudaStreamWaitEvent(gs, H.copy_done[1], 0);
     if (cudaStreamSynchronize(gs) != cudaSuccess || cudaStreamSynchronize(cs) != cudaSuccess) st = RS_ECUDA;
     return ret(st);
+}
+
+rs_status rs_deviates(int kind, uint64_t k, uint64_t L, uint64_t R, uint64_t seed, uint64_t id0,
+                      uint64_t count, uint64_t *out, void *stream)
+{
+    if (kind != 0 && kind != 1) return ret(RS_EINVAL);
+    if (L > R || (kind == 0 && k > R) || R >= (1ull << 63)) return ret(RS_EINVAL);
+    if (!have_device()) return ret(RS_ECUDA);
+    if (count == 0) return ret(RS_OK);
+    const u64 g = (count + 127) / 128;
+    k_deviates<<<(unsigned)(g < 4096 ? g : 4096), 128, 0, S(stream)>>>(kind, k, L, R, seed, id0, count, out);
+    ++t_launches;
+    return ret(cuda_ok());
 }
 
 rs_status rs_release_cache(void)

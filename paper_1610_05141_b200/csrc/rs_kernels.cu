@@ -181,40 +181,11 @@ __device__ __forceinline__ u32 skip_fast(u32 a, u32 b, float c, float m_abs, u32
 }
 
 // fp64 candidate for large mean skips (small rho: there the fp32 margin
-// m_abs = 2^-19 / |lr| fails often).  log_fast is R4's log_ (same reduction,
-// same polynomial, the general-case formula) with the IEEE division
-// f / (2 + f) replaced by an approximate reciprocal and two Newton steps, and
-// no special cases (U = u52 is normal and in (0, 1)): it differs from log_ by
-// a few ulp of |log U| <= 37, i.e. < 2^-44; the margin below allows 2^-42
-// plus 2^-48 relative for the two roundings of q, against CANON's IEEE
-// division by lr.  As with skip_fast, an uncertain floor goes to skip_exact.
-__device__ __forceinline__ double log_fast(double x)
-{
-    const double ln2_hi = 0x1.62e42fee00000p-1, ln2_lo = 0x1.a39ef35793c76p-33;
-    const double L1 = 0x1.5555555555593p-1, L2 = 0x1.999999997fa04p-2,
-                 L3 = 0x1.2492494229359p-2, L4 = 0x1.c71c51d8e78afp-3,
-                 L5 = 0x1.7466496cb03dep-3, L6 = 0x1.39a09d078c69fp-3,
-                 L7 = 0x1.2f112df3e5244p-3;
-    const u64 bits = as_bits(x);
-    const int hi = (int)(bits >> 32);
-    const int mant = hi & 0x000fffff;
-    const int half = (mant + 0x95f64) & 0x100000;
-    const int e = (hi >> 20) - 1023 + (half >> 20);
-    const double xr = from_bits(((u64)(u32)(mant | (half ^ 0x3ff00000)) << 32) | (bits & 0xffffffffull));
-    const double f = xr - 1.0, de = (double)e, d = 2.0 + f;
-    double y;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
-    y = fma(y, fma(-d, y, 1.0), y);
-    y = fma(y, fma(-d, y, 1.0), y);
-    const double s = f * y;
-    const double z = s * s;
-    const double w = z * z;
-    const double t1 = w * (L2 + w * (L4 + w * L6));
-    const double t2 = z * (L1 + w * (L3 + w * (L5 + w * L7)));
-    const double R = t2 + t1;
-    return de * ln2_hi - ((s * (f - R) - de * ln2_lo) - f);
-}
-
+// m_abs = 2^-19 / |lr| fails often).  log_fast (rs_math.cuh) differs from
+// CANON's log_ by a few ulp of |log U| <= 37, i.e. < 2^-44; the margin below
+// allows 2^-42 plus 2^-48 relative for the two roundings of q, against
+// CANON's IEEE division by lr.  As with skip_fast, an uncertain floor goes to
+// skip_exact.
 __device__ __forceinline__ u32 skip_fast64(u32 a, u32 b, double il, double m_abs, u32 r, bool full, bool &ok)
 {
     const double q = log_fast(u52(a, b)) * il;                      // ~ log(U) / lr  (>= 0)

@@ -369,3 +369,22 @@ def test_graphs_with_workspace():
     assert np.array_equal(_np(rs.gnp(V, p, 4, ws=ws)), O.gnp(V, p, 4))
     with pytest.raises(rs.RSError):
         rs.gnm(V, m, 4, ws=ws[:16])
+
+
+# ---- split deviates one by one (HYP/HRUA, BINV/BTRS on the device) ----------
+
+DEV_CASES = [(16, 50, 100), (17, 10 ** 6, 2 * 10 ** 6), (1000, 2 ** 26, 2 ** 27), (1024, 2 ** 25 + 3, 2 ** 26 + 7),
+             (5000, 3, 10 ** 4), (8192, 2 ** 40, 2 ** 41), (2 ** 20, 2 ** 45, 2 ** 46 + 1),
+             (2 ** 32, 2 ** 47, 2 ** 48), (3 * 2 ** 30, 2 ** 31, 2 ** 32), (10 ** 5, 123456, 10 ** 6),
+             (2 ** 33, 2 ** 61, 2 ** 62 - 5)]
+
+
+@pytest.mark.parametrize("k,L,R", DEV_CASES)
+def test_deviates_vs_oracle(k, L, R):
+    cnt = 20000
+    for kind, f in ((0, O.hgd_batch), (1, O.bin_batch)):
+        if kind == 1 and k > 2 ** 40:
+            continue
+        got = _np(rs.deviates(kind, k, L, R, 77, 1, cnt))
+        exp = f(k, L, R, 77, 1, cnt)
+        assert np.array_equal(got, exp), (kind, k, L, R, int(np.sum(got != exp)))
