@@ -284,7 +284,12 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         la.spill_n = spill_n;
         la.spill = spill_n + 1;
         cudaMemsetAsync(spill_n, 0, 4, st);
-        void (*wk)(LeafArgs) = wr ? k_leaf_warp_wr : p.gV ? k_leaf_warp_gnm : k_leaf_warp_wor;
+        // leaves with many duplicates (r <= 2^21: >= 22 % of leaves) top the
+        // distinct set up draw by draw instead of re-running a full round
+        const bool tu = p.r_max <= WL_TU_RMAX;
+        void (*wk)(LeafArgs) = wr ? k_leaf_warp_wr
+                             : p.gV ? (tu ? k_leaf_warp_gnm_tu : k_leaf_warp_gnm)
+                                    : (tu ? k_leaf_warp_wor_tu : k_leaf_warp_wor);
         const size_t wsm = sizeof(WarpLeaf) * WL_WARPS;
         const u64 wgrid = (p.nleaves + WL_WARPS - 1) / WL_WARPS;
         const unsigned g1 = leaf_grid((const void *)wk, 32 * WL_WARPS, wsm, wgrid);

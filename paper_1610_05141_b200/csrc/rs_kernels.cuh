@@ -151,6 +151,9 @@ constexpr int WB_WARPS = 8;
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm(LeafArgs a);
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu(LeafArgs a);
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm_tu(LeafArgs a);
+constexpr u64 WL_TU_RMAX = 1ull << 21;    // leaf ranges up to this take the top-up kernels
 // Warp-per-leaf bitmap kernels for leaf ranges r <= 2^15 (rs_leaf_bitmap.cuh).
 __global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_wor(LeafArgs a);
 __global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_comp(LeafArgs a);

@@ -291,7 +291,8 @@ __device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const RoundKeys &K, con
 }
 
 // Steps 4-6 for E positions per lane.  Returns 0 (leaf stored) or, for WOR
-// with too few distinct values, the next round's draw count J' > J.
+// with too few distinct values, WL_TOPUP | |S| (the distinct values are
+// compacted in sh.keys[h, h + |S|) for wl_topup).
 // Graph calls (NEXT-3): positions [h, h + k) of sh.keys hold the leaf's
 // sorted offsets; decode each to its packed edge (edge_pack, rs_math.cuh) in a
 // non-unrolled loop so the kernel holds a single copy of the decode.
@@ -303,7 +304,61 @@ __device__ __noinline__ void wl_store_edges(const WarpLeaf &sh, u64 *d0, u32 h, 
     __syncwarp();
 }
 
-template <int E, bool WR, bool GR>
+// WOR leaves whose round ended with |S| = dist < k distinct values (R7):
+// instead of a new full round over J + (k - dist) draws, the distinct values
+// (sorted, sh.keys[h, h + dist)) are topped up draw by draw -- draws J, J+1,
+// ... in order, each kept iff it is in neither the sorted set (binary search,
+// broadcast loads) nor the new values so far -- until k are distinct: the
+// same first-k-distinct set.  The merged run is stored directly (old value i
+// moves up by the number of new values below it).  Up to 32 new values (one
+// per lane); more returns false and the caller runs the full round.
+template <bool GR>
+__device__ __forceinline__ bool wl_topup(const WarpLeaf &sh, const RoundKeys &K, const WDrawer &dr, u32 J, u32 k,
+                                      u32 dist, u32 h, u64 base, u64 *d0, u32 lane, u64 gV)
+{
+    const u32 need = k - dist;
+    if (need > 32u) return false;
+    const u32 *ks = sh.keys + h;
+    u32 nv = 0, mv = 0xffffffffu, mr = 0;            // lane t < nv: t-th new value and its rank in ks
+    for (u32 j0 = J; nv < need; j0 += 32) {
+        u32 v[4];
+        dr.block(K, (j0 + lane) >> 2, v);
+        const u32 w = (j0 + lane) & 3u;
+        const u32 xl = w == 0 ? v[0] : w == 1 ? v[1] : w == 2 ? v[2] : v[3];
+        for (u32 t = 0; t < 32 && nv < need; ++t) {
+            const u32 x = __shfl_sync(0xffffffffu, xl, t);
+            u32 lo = 0, hi = dist;                       // lower_bound(ks, x)
+            while (lo < hi) {
+                const u32 mid = (lo + hi) >> 1;
+                if (ks[mid] < x) lo = mid + 1; else hi = mid;
+            }
+            const bool old = lo < dist && ks[lo] == x;
+            const bool dup = __any_sync(0xffffffffu, lane < nv && mv == x);
+            if (!old && !dup) {
+                if (lane == nv) { mv = x; mr = lo; }
+                ++nv;
+            }
+        }
+    }
+    // merged positions: old value i -> i + #{new < ks[i]}; new value t ->
+    // rank_t + #{new < value_t}
+    for (u32 i0 = 0; i0 < dist; i0 += 32) {         // warp-uniform trip count (shuffles inside)
+        const u32 i = i0 + lane;
+        const u32 x = i < dist ? ks[i] : 0u;
+        u32 sft = 0;
+        for (u32 t = 0; t < nv; ++t) sft += __shfl_sync(0xffffffffu, mv, t) < x;
+        if (i < dist) d0[h + i + sft] = out_word_t<GR>(base + x, gV);
+    }
+    u32 sft = 0;
+    for (u32 t = 0; t < nv; ++t) sft += __shfl_sync(0xffffffffu, mv, t) < mv;
+    if (lane < nv) d0[h + mr + sft] = out_word_t<GR>(base + mv, gV);
+    __syncwarp();
+    return true;
+}
+
+constexpr u32 WL_TOPUP = 0x80000000u;      // wl_finish: "dist distinct values compacted, top up"
+
+template <int E, bool WR, bool GR, bool TU>
 __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 P_, u64 base,
                                          u64 *dst, u32 lane, u64 gV)
 {
@@ -365,8 +420,8 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
             const u32 ndup = __reduce_add_sync(0xffffffffu, nd);
             if (ndup) {
                 const u32 dist = J - ndup;       // |S| after this round
-                if (dist < k) return J + (k - dist);
-                // compact the k distinct values through shared memory, then store
+                if (!TU && dist < k) return J + (k - dist);
+                // compact the distinct values through shared memory, then store
                 u32 keep = 0;
 #pragma unroll
                 for (int i = 0; i < E; ++i) {
@@ -381,6 +436,7 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
                     if (p >= h && p < h + J && !(p > h && y[i] == (i ? y[i - 1] : prv))) sh.keys[o++] = y[i];
                 }
                 __syncwarp();
+                if (dist < k) return WL_TOPUP | dist;      // the caller tops the set up (wl_topup)
                 if (GR) { wl_store_edges(sh, d0, h, k, base, gV, lane); return 0; }
                 const u32 ng = (h + k + 3) >> 2;
                 for (u32 g = lane; g < ng; g += 32) {
@@ -448,7 +504,7 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
     return 0;
 }
 
-template <bool WR, bool GR>
+template <bool WR, bool GR, bool TU>
 __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -498,7 +554,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
                     wl_scatter(sh, a.rk, dr, J, h, shb, lane);
                     RS_TS(ts1);
                     RS_ACC(2, ts0, ts1);
-                    res = wl_finish<WL_E1, WR, GR>(sh, J, k, h, P, base, dst, lane, a.gV);
+                    res = wl_finish<WL_E1, WR, GR, TU>(sh, J, k, h, P, base, dst, lane, a.gV);
                     RS_TS(ts2);
                     RS_ACC(5, ts1, ts2);
                 } else {
@@ -507,7 +563,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
                     __syncwarp();
 #else
                     wl_scatter(sh, a.rk, dr, J, h, shb, lane);
-                    res = wl_finish<WL_E2, WR, GR>(sh, J, k, h, P, base, dst, lane, a.gV);
+                    res = wl_finish<WL_E2, WR, GR, TU>(sh, J, k, h, P, base, dst, lane, a.gV);
 #endif
                 }
             }
@@ -516,14 +572,22 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
                 if (lane == 0) a.spill[atomicAdd(a.spill_n, 1u)] = (u32)L;
                 break;
             }
+            if (TU && (res & WL_TOPUP)) {       // |S| < k: top up draw by draw, else a full round
+                const u32 dist = res & ~WL_TOPUP;
+                if (wl_topup<GR>(sh, a.rk, dr, J, k, dist, h, base, dst - h, lane, a.gV)) break;
+                res = J + (k - dist);
+            }
             J = res;
         }
     }
 }
 
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor(LeafArgs a) { warp_leaves<false, false>(a); }
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr(LeafArgs a) { warp_leaves<true, false>(a); }
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor(LeafArgs a) { warp_leaves<false, false, false>(a); }
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr(LeafArgs a) { warp_leaves<true, false, false>(a); }
+// small leaf ranges (many duplicates): the top-up instead of full rounds
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu(LeafArgs a) { warp_leaves<false, false, true>(a); }
 // G(n, m) (NEXT-3): the WOR kernel with the edge decode fused into its stores
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm(LeafArgs a) { warp_leaves<false, true>(a); }
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm(LeafArgs a) { warp_leaves<false, true, false>(a); }
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm_tu(LeafArgs a) { warp_leaves<false, true, true>(a); }
 
 }  // namespace rs
