@@ -229,8 +229,12 @@ rs_status rs_device_errors(int clear, unsigned *flags);
  * RS_OPT_LEAF_PATH: 0 = automatic (default: warp-per-leaf kernels, bitmap
  * kernels for leaf ranges <= 2^15, CTA kernel for leaves that do not fit);
  * 1 = the CTA-per-leaf kernels for every leaf (so tests cover that path).
- * Results are identical for every setting.  Unknown option -> RS_EINVAL. */
-enum { RS_OPT_LEAF_PATH = 1 };
+ * RS_OPT_TOPUP_MAX: 0..32, most duplicates the warp kernels for small leaf
+ * ranges top up draw by draw before running a full extra round (default 32;
+ * tests lower it to cover the fallback).
+ * Results are identical for every setting.  Unknown option or value ->
+ * RS_EINVAL. */
+enum { RS_OPT_LEAF_PATH = 1, RS_OPT_TOPUP_MAX = 2 };
 rs_status rs_set_option(int option, int value);
 
 /* Number of kernel launches issued by this thread since the last reset. */

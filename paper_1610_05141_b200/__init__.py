@@ -296,6 +296,7 @@ def device_errors(clear: bool = True) -> int:
 
 
 OPT_LEAF_PATH = 1
+OPT_TOPUP_MAX = 2
 
 
 def node_info(mode: int, N: int, n: int, seed: int, depth: int, index: int):

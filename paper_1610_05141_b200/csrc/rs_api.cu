@@ -18,6 +18,7 @@ namespace {
 
 thread_local rs_status t_last = RS_OK;
 int g_leaf_path = 0;                    // rs_set_option(RS_OPT_LEAF_PATH)
+int g_topup_max = 32;                   // rs_set_option(RS_OPT_TOPUP_MAX)
 thread_local uint64_t t_launches = 0;
 
 rs_status ret(rs_status s) { t_last = s; return s; }
@@ -287,6 +288,7 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         // leaves with many duplicates (r <= 2^21: >= 22 % of leaves) top the
         // distinct set up draw by draw instead of re-running a full round
         const bool tu = p.r_max <= WL_TU_RMAX;
+        la.topup_max = (u32)g_topup_max;
         void (*wk)(LeafArgs) = wr ? k_leaf_warp_wr
                              : p.gV ? (tu ? k_leaf_warp_gnm_tu : k_leaf_warp_gnm)
                                     : (tu ? k_leaf_warp_wor_tu : k_leaf_warp_wor);
@@ -945,6 +947,10 @@ rs_status rs_set_option(int option, int value)
 {
     if (option == RS_OPT_LEAF_PATH && (value == 0 || value == 1)) {
         g_leaf_path = value;
+        return ret(RS_OK);
+    }
+    if (option == RS_OPT_TOPUP_MAX && value >= 0 && value <= 32) {
+        g_topup_max = value;
         return ret(RS_OK);
     }
     return ret(RS_EINVAL);

@@ -128,6 +128,7 @@ struct LeafArgs {
     const u32 *list_n;
     RoundKeys rk;          // Philox round keys of seed (round_keys(seed))
     u64 gV;                // != 0: graph calls, store packed edges of G(gV, .) (NEXT-3)
+    u32 topup_max;         // warp *_tu kernels: most new values topped up per leaf (<= 32)
 };
 
 __global__ void __launch_bounds__(LEAF_NT) k_leaf_wor32(LeafArgs a);

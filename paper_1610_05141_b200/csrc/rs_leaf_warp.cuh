@@ -311,13 +311,15 @@ __device__ __noinline__ void wl_store_edges(const WarpLeaf &sh, u64 *d0, u32 h, 
 // broadcast loads) nor the new values so far -- until k are distinct: the
 // same first-k-distinct set.  The merged run is stored directly (old value i
 // moves up by the number of new values below it).  Up to 32 new values (one
-// per lane); more returns false and the caller runs the full round.
+// per lane; at most LeafArgs::topup_max); more returns false and the caller
+// runs the full round.
 template <bool GR>
 __device__ __forceinline__ bool wl_topup(const WarpLeaf &sh, const RoundKeys &K, const WDrawer &dr, u32 J, u32 k,
-                                      u32 dist, u32 h, u64 base, u64 *d0, u32 lane, u64 gV)
+                                      u32 dist, u32 h, u64 base, u64 *d0, u32 lane, u64 gV, u32 tmax)
 {
     const u32 need = k - dist;
-    if (need > 32u) return false;
+    if (need > tmax) return false;                   // tmax <= 32
+
     const u32 *ks = sh.keys + h;
     u32 nv = 0, mv = 0xffffffffu, mr = 0;            // lane t < nv: t-th new value and its rank in ks
     for (u32 j0 = J; nv < need; j0 += 32) {
@@ -574,7 +576,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
             }
             if (TU && (res & WL_TOPUP)) {       // |S| < k: top up draw by draw, else a full round
                 const u32 dist = res & ~WL_TOPUP;
-                if (wl_topup<GR>(sh, a.rk, dr, J, k, dist, h, base, dst - h, lane, a.gV)) break;
+                if (wl_topup<GR>(sh, a.rk, dr, J, k, dist, h, base, dst - h, lane, a.gV, a.topup_max)) break;
                 res = J + (k - dist);
             }
             J = res;

@@ -106,6 +106,10 @@ def test_no_cpu_fallback():
 def test_set_option_host_only():
     rs.set_option(rs.OPT_LEAF_PATH, 1)
     rs.set_option(rs.OPT_LEAF_PATH, 0)
+    rs.set_option(rs.OPT_TOPUP_MAX, 0)
+    rs.set_option(rs.OPT_TOPUP_MAX, 32)
+    with pytest.raises(rs.RSError):
+        rs.set_option(rs.OPT_TOPUP_MAX, 33)
     with pytest.raises(rs.RSError):
         rs.set_option(99, 0)
     with pytest.raises(rs.RSError):

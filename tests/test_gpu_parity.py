@@ -388,3 +388,18 @@ def test_deviates_vs_oracle(k, L, R):
         got = _np(rs.deviates(kind, k, L, R, 77, 1, cnt))
         exp = f(k, L, R, 77, 1, cnt)
         assert np.array_equal(got, exp), (kind, k, L, R, int(np.sum(got != exp)))
+
+
+@pytest.mark.parametrize("tmax", [0, 1, 2])
+def test_topup_fallback(tmax):
+    # small leaf ranges: the *_tu kernels top the distinct set up draw by draw;
+    # a low limit forces the full-round fallback -- same result either way
+    rs.set_option(rs.OPT_TOPUP_MAX, tmax)
+    try:
+        for N, n in ((2 ** 30, 2 ** 20), (2 ** 26 + 12345, 2 ** 16 + 7)):
+            got = _np(rs.sample_wor(N, n, 11))
+            assert np.array_equal(got, O.sample_wor(N, n, 11)), (tmax, N, n)
+        assert np.array_equal(_np(rs.gnm(70000, 2 ** 22, 5)), O.gnm(70000, 2 ** 22, 5))
+    finally:
+        rs.set_option(rs.OPT_TOPUP_MAX, 32)
+    _no_device_errors()
