@@ -342,14 +342,18 @@ __device__ __forceinline__ bool wl_topup(const WarpLeaf &sh, const RoundKeys &K,
             }
         }
     }
-    // merged positions: old value i -> i + #{new < ks[i]}; new value t ->
-    // rank_t + #{new < value_t}
+    // merged positions: old value i -> i + #{new < ks[i]} = i + #{t : rank_t <= i}
+    // (rank_t = lower_bound of new value t in ks); new value t -> rank_t +
+    // #{new < value_t}.  The first four ranks are broadcast once.
+    const u32 r0 = __shfl_sync(0xffffffffu, lane < nv ? mr : 0xffffffffu, 0);
+    const u32 r1 = __shfl_sync(0xffffffffu, lane < nv ? mr : 0xffffffffu, 1);
+    const u32 r2 = __shfl_sync(0xffffffffu, lane < nv ? mr : 0xffffffffu, 2);
+    const u32 r3 = __shfl_sync(0xffffffffu, lane < nv ? mr : 0xffffffffu, 3);
     for (u32 i0 = 0; i0 < dist; i0 += 32) {         // warp-uniform trip count (shuffles inside)
         const u32 i = i0 + lane;
-        const u32 x = i < dist ? ks[i] : 0u;
-        u32 sft = 0;
-        for (u32 t = 0; t < nv; ++t) sft += __shfl_sync(0xffffffffu, mv, t) < x;
-        if (i < dist) d0[h + i + sft] = out_word_t<GR>(base + x, gV);
+        u32 sft = (r0 <= i) + (r1 <= i) + (r2 <= i) + (r3 <= i);
+        for (u32 t = 4; t < nv; ++t) sft += __shfl_sync(0xffffffffu, mr, t) <= i;
+        if (i < dist) d0[h + i + sft] = out_word_t<GR>(base + ks[i], gV);
     }
     u32 sft = 0;
     for (u32 t = 0; t < nv; ++t) sft += __shfl_sync(0xffffffffu, mv, t) < mv;
