@@ -13,7 +13,7 @@ import bench  # noqa: E402
 
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 out = {}
-for w in ["headline", "cfg1", "complement", "wr", "bernoulli"]:
+for w in ["headline", "cfg1", "complement", "wr", "bernoulli", "gnm", "algb"]:
     rep = os.path.join(ROOT, "gpurun_out", f"full_{w}.ncu-rep")
     if not os.path.exists(rep):
         continue
