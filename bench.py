@@ -385,7 +385,24 @@ def run_native(args):
             traffic = float(t["bytes_per_launch"]) if t else None
     except Exception:
         pass
+    # write-only ceiling on the same buffer: torch's vectorised fill of the
+    # output (untimed by the step; a store-only path's honest denominator)
+    fill_gbs = None
+    try:
+        view = out.view(torch.int64)
+        view.fill_(1)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(3):
+            view.fill_(1)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        fill_gbs = 3 * 8.0 * view.numel() / (f0.elapsed_time(f1) / 1e3) / 1e9
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "fill_ceiling": fill_gbs,
+                "frac_of_fill": (achieved / fill_gbs) if (achieved and fill_gbs) else None,
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "kernel": kname, "kernel_ms": kms_per, "peak_source": peak_src,
                 "step_share": kms / max(args.steps, 1) / ms if ms > 0 else None,
