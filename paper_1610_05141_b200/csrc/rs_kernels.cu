@@ -367,26 +367,31 @@ __device__ __forceinline__ void bern_write(const BernArgs &a, u64 tk, const B *b
 
 constexpr u64 B_AGG = 1ull << 62, B_INC = 2ull << 62, B_VAL = (1ull << 62) - 1;
 
+#ifndef RS_BSC
+#define RS_BSC 8
+#endif
 // The scanner: turns the published ticket counts (AGG) into inclusive
-// prefixes (INC) in ticket order, 256 tickets per step.
+// prefixes (INC) in ticket order, 32 * RS_BSC tickets per step (one L2
+// round trip each: the scanner's step rate bounds the kernel when tickets are
+// cheap, so each lane takes RS_BSC independent loads).
 __device__ __forceinline__ void bern_scanner(const BernArgs &a, u64 ntick, u32 lane)
 {
     u64 next = 0, run = 0;
     while (next < ntick) {
-        u64 v[8];
-        u32 fu = 8;                                    // first unpublished entry of the lane
+        u64 v[RS_BSC];
+        u32 fu = RS_BSC;                                    // first unpublished entry of the lane
 #pragma unroll
-        for (int i = 7; i >= 0; --i) {
-            const u64 idx = next + 8 * lane + i;
+        for (int i = RS_BSC - 1; i >= 0; --i) {
+            const u64 idx = next + RS_BSC * lane + i;
             v[i] = idx < ntick ? ld_relaxed(a.status + idx) : 0ull;
             if (idx >= ntick || (v[i] >> 62) == 0) fu = i;
         }
-        const u32 first = __reduce_min_sync(0xffffffffu, fu == 8 ? 0xffffffffu : 8 * lane + fu);
-        const u32 np = first == 0xffffffffu ? 256u : first;   // consecutive published tickets
+        const u32 first = __reduce_min_sync(0xffffffffu, fu == RS_BSC ? 0xffffffffu : RS_BSC * lane + fu);
+        const u32 np = first == 0xffffffffu ? 32u * RS_BSC : first;   // consecutive published tickets
         if (np == 0) { __nanosleep(256); continue; }
         u64 loc = 0;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) if (8 * lane + i < np) loc += v[i] & B_VAL;
+        for (int i = 0; i < RS_BSC; ++i) if (RS_BSC * lane + i < np) loc += v[i] & B_VAL;
         u64 incl = loc;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -395,10 +400,10 @@ __device__ __forceinline__ void bern_scanner(const BernArgs &a, u64 ntick, u32 l
         }
         u64 pref = run + incl - loc;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            if (8 * lane + i < np) {
+        for (int i = 0; i < RS_BSC; ++i) {
+            if (RS_BSC * lane + i < np) {
                 pref += v[i] & B_VAL;
-                st_relaxed(a.status + next + 8 * lane + i, B_INC | pref);
+                st_relaxed(a.status + next + RS_BSC * lane + i, B_INC | pref);
             }
         }
         run += __shfl_sync(0xffffffffu, incl, 31);
