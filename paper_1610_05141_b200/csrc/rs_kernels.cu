@@ -122,9 +122,9 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split(SplitArgs a) { split_top<fal
 __global__ void __launch_bounds__(SPLIT_NT) k_split_wr(SplitArgs a) { split_top<true>(a); }
 __global__ void __launch_bounds__(LEVEL_NT, RS_LV_MINB) k_split_level(LevelArgs a) { split_level<false>(a); }
 __global__ void __launch_bounds__(LEVEL_NT, RS_LV_MINB) k_split_level_wr(LevelArgs a) { split_level<true>(a); }
-__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep2(LevelArgs a) { split_deep<2, false>(a); }
+__global__ void __launch_bounds__(LEVEL_NT, RS_D3_MINB) k_split_deep2(LevelArgs a) { split_deep<2, false>(a); }
 __global__ void __launch_bounds__(LEVEL_NT, RS_D3_MINB) k_split_deep3(LevelArgs a) { split_deep<3, false>(a); }
-__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep4(LevelArgs a) { split_deep<4, false>(a); }
+__global__ void __launch_bounds__(LEVEL_NT, RS_D3_MINB) k_split_deep4(LevelArgs a) { split_deep<4, false>(a); }
 __global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep2_wr(LevelArgs a) { split_deep<2, true>(a); }
 __global__ void __launch_bounds__(LEVEL_NT, RS_D3_MINB) k_split_deep3_wr(LevelArgs a) { split_deep<3, true>(a); }
 __global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep4_wr(LevelArgs a) { split_deep<4, true>(a); }

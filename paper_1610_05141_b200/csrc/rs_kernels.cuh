@@ -105,12 +105,12 @@ struct LevelArgs {
 __global__ void __launch_bounds__(LEVEL_NT, RS_LV_MINB) k_split_level(LevelArgs a);
 __global__ void __launch_bounds__(LEVEL_NT, RS_LV_MINB) k_split_level_wr(LevelArgs a);
 // The last 2, 3 or 4 levels in one launch, a thread per subtree.
-__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep2(LevelArgs a);
 #ifndef RS_D3_MINB
 #define RS_D3_MINB 8      // 64 registers: twice the warps (measured: split 1.66 -> 1.49 ms)
 #endif
+__global__ void __launch_bounds__(LEVEL_NT, RS_D3_MINB) k_split_deep2(LevelArgs a);
 __global__ void __launch_bounds__(LEVEL_NT, RS_D3_MINB) k_split_deep3(LevelArgs a);
-__global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep4(LevelArgs a);
+__global__ void __launch_bounds__(LEVEL_NT, RS_D3_MINB) k_split_deep4(LevelArgs a);
 __global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep2_wr(LevelArgs a);
 __global__ void __launch_bounds__(LEVEL_NT, RS_D3_MINB) k_split_deep3_wr(LevelArgs a);
 __global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep4_wr(LevelArgs a);
