@@ -325,10 +325,11 @@ def run_native(args):
     if mode == "bernoulli":
         c_local = min(int(cnt.item()), local_cap) if args.no_check else int(cnt.item())
         assert c_local <= local_cap, "bernoulli capacity exceeded"
-        bad = rs.validate(out[:c_local], N, strict=True)
+        bad = 0 if args.launch_list else rs.validate(out[:c_local], N, strict=True)
         n_local_done = c_local
     else:
-        bad = rs.validate(out[:n_local], 2 ** 64 - 1 if mode == "gnm" else N, strict=(mode != "wr"))
+        bad = 0 if args.launch_list else rs.validate(out[:n_local], 2 ** 64 - 1 if mode == "gnm" else N,
+                                                     strict=(mode != "wr"))
         n_local_done = n_local
         if world > 1:
             off = int(allc[:rank].sum().item())
@@ -389,6 +390,8 @@ def run_native(args):
     # output (untimed by the step; a store-only path's honest denominator)
     fill_gbs = None
     try:
+        if args.launch_list:
+            raise RuntimeError("skipped")
         view = out.view(torch.int64)
         view.fill_(1)
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -477,6 +480,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-check", action="store_true", help="dev: skip the output validation asserts")
+    ap.add_argument("--launch-list", action="store_true",
+                    help="only the step's kernels (no validation / fill-ceiling kernels): for the ncu launch list")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: smoke-test the N > 1 path with ranks sharing one GPU")
     args = ap.parse_args()

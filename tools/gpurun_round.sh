@@ -10,6 +10,6 @@ timeout 1500 python -m pytest tests -m gpu -q --timeout 400 > gpurun_out/pytest_
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_reference.log 2>&1; echo "rc=$?" >> gpurun_out/bench_reference.log
 for w in cfg1 complement wr bernoulli bernoulli32 cfg0 gnm algb; do timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --workload $w > gpurun_out/bench_$w.log 2>&1; echo "rc=$?" >> gpurun_out/bench_$w.log; done
-timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/plain_launch.log 2>&1 && \
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_launch.log 2>&1
+timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --launch-list > gpurun_out/plain_launch.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --launch-list > gpurun_out/ncu_launch.log 2>&1
 tail -n 2 gpurun_out/smoke.log gpurun_out/pytest_gpu.log gpurun_out/bench.log
