@@ -15,6 +15,9 @@ constexpr int SPLIT_LEVELS = 11;                 // levels expanded per split ph
 constexpr int SPLIT_WIDTH = 1 << SPLIT_LEVELS;   // nodes per CTA at the phase's last level
 
 constexpr int LEAF_NT = 512;                     // threads per leaf CTA
+#ifndef RS_LEAF_MINB
+#define RS_LEAF_MINB 2      // 2 CTAs per SM (64 registers): wide leaves 15 % faster
+#endif
 constexpr int LEAF_CAP = 2048;                   // draws held on chip per leaf
 constexpr int LEAF_EPT = LEAF_CAP / LEAF_NT;     // elements per thread
 
@@ -137,12 +140,12 @@ struct LeafArgs {
     u32 topup_max;         // warp *_tu kernels: most new values topped up per leaf (<= 32)
 };
 
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_wor32(LeafArgs a);
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_wor64(LeafArgs a);
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_wr32(LeafArgs a);
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_wr64(LeafArgs a);
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_comp32(LeafArgs a);
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_comp64(LeafArgs a);
+__global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_wor32(LeafArgs a);
+__global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_wor64(LeafArgs a);
+__global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_wr32(LeafArgs a);
+__global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_wr64(LeafArgs a);
+__global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_comp32(LeafArgs a);
+__global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_comp64(LeafArgs a);
 
 // Warp-per-leaf kernels (u32 keys): the common path; see rs_leaf.cuh.
 #ifndef RS_WL_MINB

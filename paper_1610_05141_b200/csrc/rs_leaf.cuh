@@ -433,10 +433,10 @@ __device__ __forceinline__ void sample_leaves(const LeafArgs &a)
     }
 }
 
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_wor32(LeafArgs a) { sample_leaves<u32, false>(a); }
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_wor64(LeafArgs a) { sample_leaves<u64, false>(a); }
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_wr32(LeafArgs a) { sample_leaves<u32, true>(a); }
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_wr64(LeafArgs a) { sample_leaves<u64, true>(a); }
+__global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_wor32(LeafArgs a) { sample_leaves<u32, false>(a); }
+__global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_wor64(LeafArgs a) { sample_leaves<u64, false>(a); }
+__global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_wr32(LeafArgs a) { sample_leaves<u32, true>(a); }
+__global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_wr64(LeafArgs a) { sample_leaves<u64, true>(a); }
 
 // Complement leaves (a7): the leaf's output is [lo, lo + r) minus
 // the e excluded values of the core leaf.  Work item = (leaf, window of
@@ -511,7 +511,7 @@ __device__ __forceinline__ void complement_leaves(const LeafArgs &a)
     }
 }
 
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_comp32(LeafArgs a) { complement_leaves<u32>(a); }
-__global__ void __launch_bounds__(LEAF_NT) k_leaf_comp64(LeafArgs a) { complement_leaves<u64>(a); }
+__global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_comp32(LeafArgs a) { complement_leaves<u32>(a); }
+__global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_comp64(LeafArgs a) { complement_leaves<u64>(a); }
 
 }  // namespace rs
