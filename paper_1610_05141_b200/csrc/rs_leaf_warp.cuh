@@ -30,6 +30,9 @@
 // Leaves that do not fit (J + h > 32 * WL_E2, or a bucket load above WL_PMAX)
 // are appended to a spill list that the CTA kernel (rs_leaf.cuh) completes.
 
+#ifndef RS_WL_SMEMST
+#define RS_WL_SMEMST 1      // base / output pointer through shared memory (measured 14.03 -> 13.74 ms)
+#endif
 #ifndef RS_WL_MINB
 #define RS_WL_MINB 1          // resident CTAs per SM the register budget is sized for (16 warps)
 #endif
@@ -61,6 +64,9 @@ struct WarpLeaf {
     u32 cnt[WL_B + WL_B / 32];             // padded bucket counters / starts (33 words per lane)
     unsigned long long pf_off;             // prefetched count / offset of the warp's next leaf
     u32 pf_k, pf_pad;                      //   (in shared memory: not live in registers)
+#if RS_WL_SMEMST
+    unsigned long long cur_base, cur_dst;  // the current leaf's base value / output pointer
+#endif
     u32 keys[WL_CAP];                      // staging (draw order), then positions: pad, draws, sentinels
 };
 
@@ -366,7 +372,7 @@ constexpr u32 WL_TOPUP = 0x80000000u;      // wl_finish: "dist distinct values c
 
 template <int E, bool WR, bool GR, bool TU>
 __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 P_, u64 base,
-                                         u64 *dst, u32 lane, u64 gV)
+                                         u64 *dst, u32 lane, u64 gV)   // (base, dst: unused if RS_WL_SMEMST)
 {
     u32 P = P_;
     RS_TS(tf0);
@@ -403,6 +409,11 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
     RS_TS(tf1);
     RS_ACC(3, tf0, tf1);
     const u32 p0 = E * lane;
+#if RS_WL_SMEMST
+    // reloaded here (not live in registers through the count/scatter/sort)
+    base = sh.cur_base;
+    dst = reinterpret_cast<u64 *>(sh.cur_dst);
+#endif
     u64 *d0 = dst - h;                           // 32-byte aligned
     if (!WR) {
         // 5. duplicates = equal neighbours (Algorithm H rejects them).  Fast
@@ -542,14 +553,26 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
         if (k == 0) continue;
         const LeafGeom g = leaf_geom(a, L);
         const int cr = ceil_log2(g.r);
+#if RS_WL_SMEMST < 2
         const WDrawer dr(Stream(a.seed, WR ? P_WR : P_WOR, g.id), g.r, cr);
+#endif
         u64 *dst = a.out + off;
         const u32 h = (u32)(reinterpret_cast<uintptr_t>(dst) >> 3) & 3u;
         const int shb = cr > WL_LOGB ? cr - WL_LOGB : 0;
         const u64 base = g.lo + 1;
+#if RS_WL_SMEMST
+        if (lane == 0) { sh.cur_base = base; sh.cur_dst = reinterpret_cast<unsigned long long>(dst); }
+        __syncwarp();
+#endif
         u32 J = k;
         for (;;) {
             u32 res = 0xffffffffu;
+#if RS_WL_SMEMST >= 2
+            // the drawer is rebuilt per round (from L) rather than held live
+            // through the sort and stores
+            const LeafGeom g2 = leaf_geom(a, L);
+            const WDrawer dr(Stream(a.seed, WR ? P_WR : P_WOR, g2.id), g2.r, ceil_log2(g2.r));
+#endif
             if (J + h <= (u32)WL_CAP) {
                 const u32 P = wl_count(sh, a.rk, dr, J, shb, lane);
                 if (P > WL_PMAX) {              // pathological bucket load
@@ -560,7 +583,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
                     wl_scatter(sh, a.rk, dr, J, h, shb, lane);
                     RS_TS(ts1);
                     RS_ACC(2, ts0, ts1);
-                    res = wl_finish<WL_E1, WR, GR, TU>(sh, J, k, h, P, base, dst, lane, a.gV);
+                    res = wl_finish<WL_E1, WR, GR, TU>(sh, J, k, h, P, RS_WL_SMEMST ? 0 : base, RS_WL_SMEMST ? nullptr : dst, lane, a.gV);
                     RS_TS(ts2);
                     RS_ACC(5, ts1, ts2);
                 } else {
