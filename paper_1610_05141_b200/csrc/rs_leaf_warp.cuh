@@ -553,9 +553,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
         if (k == 0) continue;
         const LeafGeom g = leaf_geom(a, L);
         const int cr = ceil_log2(g.r);
-#if RS_WL_SMEMST < 2
         const WDrawer dr(Stream(a.seed, WR ? P_WR : P_WOR, g.id), g.r, cr);
-#endif
         u64 *dst = a.out + off;
         const u32 h = (u32)(reinterpret_cast<uintptr_t>(dst) >> 3) & 3u;
         const int shb = cr > WL_LOGB ? cr - WL_LOGB : 0;
@@ -567,12 +565,6 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
         u32 J = k;
         for (;;) {
             u32 res = 0xffffffffu;
-#if RS_WL_SMEMST >= 2
-            // the drawer is rebuilt per round (from L) rather than held live
-            // through the sort and stores
-            const LeafGeom g2 = leaf_geom(a, L);
-            const WDrawer dr(Stream(a.seed, WR ? P_WR : P_WOR, g2.id), g2.r, ceil_log2(g2.r));
-#endif
             if (J + h <= (u32)WL_CAP) {
                 const u32 P = wl_count(sh, a.rk, dr, J, shb, lane);
                 if (P > WL_PMAX) {              // pathological bucket load
