@@ -33,6 +33,9 @@
 #ifndef RS_WL_SMEMST
 #define RS_WL_SMEMST 1      // base / output pointer through shared memory (measured 14.03 -> 13.74 ms)
 #endif
+#ifndef RS_WL_RANK
+#define RS_WL_RANK 0        // count atomics return the rank in the bucket (u8 per draw); the scatter reads start + rank
+#endif
 #ifndef RS_WL_MINB
 #define RS_WL_MINB 1          // resident CTAs per SM the register budget is sized for (16 warps)
 #endif
@@ -68,6 +71,9 @@ struct WarpLeaf {
     unsigned long long cur_base, cur_dst;  // the current leaf's base value / output pointer
 #endif
     u32 keys[WL_CAP];                      // staging (draw order), then positions: pad, draws, sentinels
+#if RS_WL_RANK
+    u32 rank[WL_CAP / 4];                  // draw j's rank in its bucket: byte j & 3 of word j >> 2
+#endif
 };
 
 // Word of bucket b's counter.  Lane l owns buckets [32 l, 32 l + 32) for the
@@ -151,6 +157,27 @@ __device__ __forceinline__ u32 wl_count(WarpLeaf &sh, const RoundKeys &K, const 
         u32 v[4], v2[4];
         dr.block(K, q, v);
         dr.block(K, q2, v2);
+#if RS_WL_RANK && !defined(RS_WL_REGEN)
+        // ATOMS with return: the old count is the draw's rank in its bucket
+        // (ranks above 255 wrap, but then the bucket load exceeds WL_PMAX and
+        // the leaf spills before the ranks are read)
+        u32 rk = 0, rk2 = 0;
+        if (q2 < qfull) {
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                rk |= (atomicAdd(&sh.cnt[wl_word(v[w] >> shb)], 1u) & 0xffu) << (8 * w);
+                rk2 |= (atomicAdd(&sh.cnt[wl_word(v2[w] >> shb)], 1u) & 0xffu) << (8 * w);
+            }
+        } else {
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                if (4 * q + w < J) rk |= (atomicAdd(&sh.cnt[wl_word(v[w] >> shb)], 1u) & 0xffu) << (8 * w);
+                if (4 * q2 + w < J) rk2 |= (atomicAdd(&sh.cnt[wl_word(v2[w] >> shb)], 1u) & 0xffu) << (8 * w);
+            }
+        }
+        sh.rank[q] = rk;
+        if (q2 < nq) sh.rank[q2] = rk2;
+#else
         if (q2 < qfull) {
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
@@ -166,6 +193,7 @@ __device__ __forceinline__ u32 wl_count(WarpLeaf &sh, const RoundKeys &K, const 
                 if (4 * q2 + w < J) atomicAdd(&sh.cnt[wl_word(v2[w] >> shb)], 1u);
             }
         }
+#endif
 #if !defined(RS_WL_REGEN)
         *reinterpret_cast<uint4 *>(&sh.keys[4 * q]) = make_uint4(v[0], v[1], v[2], v[3]);
         if (q2 < nq) *reinterpret_cast<uint4 *>(&sh.keys[4 * q2]) = make_uint4(v2[0], v2[1], v2[2], v2[3]);
@@ -252,15 +280,26 @@ __device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const RoundKeys &K, con
     // scatter overwrites the staging area
     constexpr int NB = WL_E1 / 4;
     u32 x[WL_E1];
+#if RS_WL_RANK
+    u32 rk[NB];
+#endif
 #pragma unroll
     for (int m = 0; m < NB; ++m) {
         const u32 q = lane + 32u * m;
         if (4 * q < J) {
             const uint4 t = *reinterpret_cast<const uint4 *>(&sh.keys[4 * q]);
             x[4 * m] = t.x; x[4 * m + 1] = t.y; x[4 * m + 2] = t.z; x[4 * m + 3] = t.w;
+#if RS_WL_RANK
+            rk[m] = sh.rank[q];
+#endif
         }
     }
     __syncwarp();
+#if RS_WL_RANK
+#define WL_POS(e) (sh.cnt[wl_word(x[e] >> shb)] + ((rk[(e) >> 2] >> (8 * ((e) & 3))) & 0xffu))
+#else
+#define WL_POS(e) atomicAdd(&sh.cnt[wl_word(x[e] >> shb)], 1u)
+#endif
     // Atomics first, stores after, in groups of GB blocks: smem stores and
     // atomics may alias as far as the compiler knows, so interleaving them
     // would serialise every atomic's round trip.
@@ -277,7 +316,7 @@ __device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const RoundKeys &K, con
 #ifdef RS_EXP_NOSCATTER
                 pos[e - 4 * m0] = 4 * (lane + 32u * (e >> 2)) + (e & 3);
 #else
-                pos[e - 4 * m0] = atomicAdd(&sh.cnt[wl_word(x[e] >> shb)], 1u);
+                pos[e - 4 * m0] = WL_POS(e);
 #endif
 #pragma unroll
             for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) kh[pos[e - 4 * m0]] = x[e];
@@ -285,13 +324,14 @@ __device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const RoundKeys &K, con
 #pragma unroll
             for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) {
                 const u32 j = 4 * (lane + 32u * (e >> 2)) + (e & 3);
-                pos[e - 4 * m0] = j < J ? atomicAdd(&sh.cnt[wl_word(x[e] >> shb)], 1u) : (u32)WL_CAP;
+                pos[e - 4 * m0] = j < J ? WL_POS(e) : (u32)WL_CAP;
             }
 #pragma unroll
             for (int e = 4 * m0; e < 4 * (m0 + GB); ++e)
                 if (pos[e - 4 * m0] != (u32)WL_CAP) kh[pos[e - 4 * m0]] = x[e];
         }
     }
+#undef WL_POS
 #endif
     __syncwarp();
 }
