@@ -36,6 +36,9 @@
 #ifndef RS_WL_RANK
 #define RS_WL_RANK 0        // count atomics return the rank in the bucket (u8 per draw); the scatter reads start + rank
 #endif
+#ifndef RS_WL_TUV4
+#define RS_WL_TUV4 0        // top-up merge stored by output slot, 32-byte stores (bit-exact; measured slower: cfg1 leaf 4.99 -> 5.56 ms)
+#endif
 #ifndef RS_WL_MINB
 #define RS_WL_MINB 1          // resident CTAs per SM the register budget is sized for (16 warps)
 #endif
@@ -388,6 +391,44 @@ __device__ __forceinline__ bool wl_topup(const WarpLeaf &sh, const RoundKeys &K,
             }
         }
     }
+#if RS_WL_TUV4
+    if (!GR && nv <= 4) {
+        // merged output slot o (0 <= o < k) holds new value t if o == F_t
+        // (F_t = rank_t + #{new < value_t}, its final position), else old value
+        // ks[o - #{t : F_t < o}].  Output by slot, four per lane: 32-byte
+        // stores on the output's 32-byte grid (d0 is aligned, slots start at h).
+        u32 F = 0xffffffffu;
+        {
+            u32 sft = 0;
+            for (u32 t = 0; t < nv; ++t) sft += __shfl_sync(0xffffffffu, mv, t) < mv;
+            if (lane < nv) F = mr + sft;
+        }
+        const u32 F0 = __shfl_sync(0xffffffffu, F, 0), F1 = __shfl_sync(0xffffffffu, F, 1);
+        const u32 F2 = __shfl_sync(0xffffffffu, F, 2), F3 = __shfl_sync(0xffffffffu, F, 3);
+        const u32 m0 = __shfl_sync(0xffffffffu, mv, 0), m1 = __shfl_sync(0xffffffffu, mv, 1);
+        const u32 m2 = __shfl_sync(0xffffffffu, mv, 2), m3 = __shfl_sync(0xffffffffu, mv, 3);
+        const u32 end = h + k, ng = (end + 3) >> 2;
+        for (u32 g = lane; g < ng; g += 32) {
+            u64 w[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const u32 o = 4 * g + t - h;       // wraps (huge) below h: F_t < o false
+                const u32 c = (F0 < o) + (F1 < o) + (F2 < o) + (F3 < o);
+                const u32 v = o == F0 ? m0 : o == F1 ? m1 : o == F2 ? m2 : o == F3 ? m3 : ks[min(o - c, (u32)WL_CAP - 1u - h)];
+                w[t] = out_word_t<GR>(base + v, gV);
+            }
+            if (4 * g >= h && 4 * g + 4 <= end) {
+                st_v4(d0 + 4 * g, w[0], w[1], w[2], w[3]);
+            } else {
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (4 * g + t >= h && 4 * g + t < end) d0[4 * g + t] = w[t];
+            }
+        }
+        __syncwarp();
+        return true;
+    }
+#endif
     // merged positions: old value i -> i + #{new < ks[i]} = i + #{t : rank_t <= i}
     // (rank_t = lower_bound of new value t in ks); new value t -> rank_t +
     // #{new < value_t}.  The first four ranks are broadcast once.

@@ -48,6 +48,8 @@ WOR_CASES = [
     (10 ** 9 + 7, 100003), (3 ** 30, 2 ** 18 + 17), (2 ** 33 + 12345, 300001),
     # dense leaves: many rounds of first-k-distinct (n = N/2 not complemented)
     (2 ** 21, 2 ** 20), (2 ** 15, 2 ** 14), (3 * 2 ** 14 + 1, 3 * 2 ** 13),
+    # top-up regime (leaf ranges 2^16..2^18: several new values per leaf, some leaves > 4)
+    (2 ** 20, 2 ** 14), (2 ** 21 + 99, 2 ** 14 + 5), (2 ** 24 + 3, 2 ** 16 + 1),
     # complement (2n > N), incl. the cfg3a shape at reduced N
     (2 ** 22, 3 * 2 ** 20), (2 ** 20 + 3, 2 ** 20), (10 ** 6, 999_000),
     # leaf ranges above 2^32 (64-bit keys)
