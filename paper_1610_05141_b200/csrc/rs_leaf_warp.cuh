@@ -306,7 +306,10 @@ __device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const RoundKeys &K, con
     // Atomics first, stores after, in groups of GB blocks: smem stores and
     // atomics may alias as far as the compiler knows, so interleaving them
     // would serialise every atomic's round trip.
-    constexpr int GB = 3;
+#ifndef RS_WL_GB
+#define RS_WL_GB 3          // measured: headline leaf 14.06 (1) / 13.66 (3) / 14.09 ms (9)
+#endif
+    constexpr int GB = RS_WL_GB;
     static_assert(NB % GB == 0, "group size");
 #pragma unroll
     for (int m0 = 0; m0 < NB; m0 += GB) {
