@@ -39,6 +39,9 @@
 #ifndef RS_WL_TUV4
 #define RS_WL_TUV4 0        // top-up merge stored by output slot, 32-byte stores (bit-exact; measured slower: cfg1 leaf 4.99 -> 5.56 ms)
 #endif
+#ifndef RS_WL_EXACTP
+#define RS_WL_EXACTP 1      // exactly P odd-even phases (not P rounded up to even)
+#endif
 #ifndef RS_WL_MINB
 #define RS_WL_MINB 1          // resident CTAs per SM the register budget is sized for (16 warps)
 #endif
@@ -480,7 +483,14 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
 #ifdef RS_EXP_NOSORT
     P = 0;
 #endif
+#if RS_WL_EXACTP
+    // a bucket of c draws is sorted after c alternating phases (c = 1: none),
+    // so exactly P phases: pairs, then a lone even phase if P is odd
+    if (P < 2) P = 0;
+    for (u32 ph = 0; ph + 1 < P; ph += 2) {      // even + odd phase per step
+#else
     for (u32 ph = 0; ph < P; ph += 2) {          // even + odd phase per step (P rounded up)
+#endif
 #pragma unroll
         for (int i = 0; i < E; i += 2) wl_ce(y[i], y[i + 1]);
         const u32 nxt = __shfl_down_sync(0xffffffffu, y[0], 1);
@@ -490,6 +500,12 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
         if (lane < 31) y[E - 1] = min(y[E - 1], nxt);
         if (lane > 0) y[0] = max(prv, y[0]);
     }
+#if RS_WL_EXACTP
+    if (P & 1) {
+#pragma unroll
+        for (int i = 0; i < E; i += 2) wl_ce(y[i], y[i + 1]);
+    }
+#endif
     RS_TS(tf1);
     RS_ACC(3, tf0, tf1);
     const u32 p0 = E * lane;
