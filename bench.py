@@ -375,7 +375,8 @@ def run_native(args):
             kname = "k_leaf_bitmap_comp" if comp else "k_leaf_bitmap_wor"
         else:
             kname = {"wr": "k_leaf_warp_wr", "gnm": "k_leaf_warp_gnm"}.get(mode, "k_leaf_warp_wor")
-            if mode != "wr" and r_max <= 2 ** 21:      # small ranges: the top-up kernels
+            # the top-up kernels: plain WOR at every range, G(n, m) for small ranges
+            if mode == "wor" or (mode == "gnm" and r_max <= 2 ** 21):
                 kname += "_tu"
     kms_per = kms / max(kl, 1)
     achieved = bytes_per_launch / (kms_per / 1e3) / 1e9 if kms_per > 0 else None

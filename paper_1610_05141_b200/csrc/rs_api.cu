@@ -292,9 +292,16 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         // distinct set up draw by draw instead of re-running a full round
         const bool tu = p.r_max <= WL_TU_RMAX;
         la.topup_max = (u32)g_topup_max;
+        // plain WOR takes the top-up kernel at every range: since the exact
+        // phase count it needs no spill slots and is faster than the plain
+        // kernel (headline leaf 13.64 -> 12.88 ms); G(n, m) keeps the cutoff
+        // (its _tu kernel measured slower above 2^21: 21.97 -> 23.64 ms)
+#ifndef RS_WL_WOR_TU_ALL
+#define RS_WL_WOR_TU_ALL 1
+#endif
         void (*wk)(LeafArgs) = wr ? k_leaf_warp_wr
                              : p.gV ? (tu ? k_leaf_warp_gnm_tu : k_leaf_warp_gnm)
-                                    : (tu ? k_leaf_warp_wor_tu : k_leaf_warp_wor);
+                                    : ((tu || RS_WL_WOR_TU_ALL) ? k_leaf_warp_wor_tu : k_leaf_warp_wor);
         const size_t wsm = sizeof(WarpLeaf) * WL_WARPS;
         const u64 wgrid = (p.nleaves + WL_WARPS - 1) / WL_WARPS;
         const unsigned g1 = leaf_grid((const void *)wk, 32 * WL_WARPS, wsm, wgrid);

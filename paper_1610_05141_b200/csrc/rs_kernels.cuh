@@ -163,7 +163,10 @@ __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr(Leaf
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm_tu(LeafArgs a);
-constexpr u64 WL_TU_RMAX = 1ull << 21;    // leaf ranges up to this take the top-up kernels
+#ifndef RS_WL_TU_LOG
+#define RS_WL_TU_LOG 21
+#endif
+constexpr u64 WL_TU_RMAX = 1ull << RS_WL_TU_LOG;   // leaf ranges up to this take the top-up kernels
 // Warp-per-leaf bitmap kernels for leaf ranges r <= 2^15 (rs_leaf_bitmap.cuh).
 __global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_wor(LeafArgs a);
 __global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_comp(LeafArgs a);
