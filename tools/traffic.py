@@ -13,6 +13,10 @@ import bench  # noqa: E402
 
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 out = {}
+try:    # entries of workloads not captured this time are kept
+    out = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+except Exception:
+    pass
 for w in ["headline", "cfg1", "complement", "wr", "bernoulli", "gnm", "algb"]:
     rep = os.path.join(ROOT, "gpurun_out", f"full_{w}.ncu-rep")
     if not os.path.exists(rep):
