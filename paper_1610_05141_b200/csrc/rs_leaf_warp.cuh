@@ -31,7 +31,7 @@
 // are appended to a spill list that the CTA kernel (rs_leaf.cuh) completes.
 
 #ifndef RS_WL_SMEMST
-#define RS_WL_SMEMST 1      // base / output pointer through shared memory (measured 14.03 -> 13.74 ms)
+#define RS_WL_SMEMST 0      // base / output pointer through shared memory (measured 14.03 -> 13.74 ms with the plain kernel; with the spill-free top-up kernel off is faster: 12.87 -> 12.64 ms)
 #endif
 #ifndef RS_WL_RANK
 #define RS_WL_RANK 0        // count atomics return the rank in the bucket (u8 per draw); the scatter reads start + rank
