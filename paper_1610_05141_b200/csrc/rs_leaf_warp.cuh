@@ -39,6 +39,9 @@
 #ifndef RS_WL_TUV4
 #define RS_WL_TUV4 0        // top-up merge stored by output slot, 32-byte stores (bit-exact; measured slower: cfg1 leaf 4.99 -> 5.56 ms)
 #endif
+#ifndef RS_WL_CB
+#define RS_WL_CB 2          // Philox blocks per count step (> 2: generic loop)
+#endif
 #ifndef RS_WL_EXACTP
 #define RS_WL_EXACTP 1      // exactly P odd-even phases (not P rounded up to even)
 #endif
@@ -157,6 +160,31 @@ __device__ __forceinline__ u32 wl_count(WarpLeaf &sh, const RoundKeys &K, const 
     RS_TS(tc0);
     const u32 qfull = J >> 2;                    // blocks whose 4 draws all count
     const u32 nq = (J + 3) >> 2;                 // blocks of the round
+#if RS_WL_CB > 2
+    // RS_WL_CB independent Philox blocks per step (ILP)
+#pragma unroll 1
+    for (u32 q0 = lane; q0 < nq; q0 += 32 * RS_WL_CB) {
+        u32 v[RS_WL_CB][4];
+#pragma unroll
+        for (int c = 0; c < RS_WL_CB; ++c) dr.block(K, q0 + 32 * c, v[c]);
+        if (q0 + 32 * (RS_WL_CB - 1) < qfull) {
+#pragma unroll
+            for (int w = 0; w < 4; ++w)
+#pragma unroll
+                for (int c = 0; c < RS_WL_CB; ++c) atomicAdd(&sh.cnt[wl_word(v[c][w] >> shb)], 1u);
+        } else {
+#pragma unroll
+            for (int w = 0; w < 4; ++w)
+#pragma unroll
+                for (int c = 0; c < RS_WL_CB; ++c)
+                    if (4 * (q0 + 32 * c) + w < J) atomicAdd(&sh.cnt[wl_word(v[c][w] >> shb)], 1u);
+        }
+#pragma unroll
+        for (int c = 0; c < RS_WL_CB; ++c)
+            if (q0 + 32 * c < nq)
+                *reinterpret_cast<uint4 *>(&sh.keys[4 * (q0 + 32 * c)]) = make_uint4(v[c][0], v[c][1], v[c][2], v[c][3]);
+    }
+#else
 #pragma unroll 1
     for (u32 q = lane; q < nq; q += 64) {        // two independent Philox blocks per step (ILP)
         const u32 q2 = q + 32;
@@ -205,6 +233,7 @@ __device__ __forceinline__ u32 wl_count(WarpLeaf &sh, const RoundKeys &K, const 
         if (q2 < nq) *reinterpret_cast<uint4 *>(&sh.keys[4 * q2]) = make_uint4(v2[0], v2[1], v2[2], v2[3]);
 #endif
     }
+#endif
     __syncwarp();
     RS_TS(tc1);
     u32 *cl = sh.cnt + 33 * lane;
