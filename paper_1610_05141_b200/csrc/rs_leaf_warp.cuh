@@ -30,6 +30,9 @@
 // Leaves that do not fit (J + h > 32 * WL_E2, or a bucket load above WL_PMAX)
 // are appended to a spill list that the CTA kernel (rs_leaf.cuh) completes.
 
+#ifndef RS_WL_SMEMST_GR
+#define RS_WL_SMEMST_GR 1   // the same, for the G(n, m) kernels only (measured gnm leaf 22.38 -> 21.99 ms)
+#endif
 #ifndef RS_WL_SMEMST
 #define RS_WL_SMEMST 0      // base / output pointer through shared memory (measured 14.03 -> 13.74 ms with the plain kernel; with the spill-free top-up kernel off is faster: 12.87 -> 12.64 ms)
 #endif
@@ -76,7 +79,7 @@ struct WarpLeaf {
     u32 cnt[WL_B + WL_B / 32];             // padded bucket counters / starts (33 words per lane)
     unsigned long long pf_off;             // prefetched count / offset of the warp's next leaf
     u32 pf_k, pf_pad;                      //   (in shared memory: not live in registers)
-#if RS_WL_SMEMST
+#if RS_WL_SMEMST || RS_WL_SMEMST_GR
     unsigned long long cur_base, cur_dst;  // the current leaf's base value / output pointer
 #endif
     u32 keys[WL_CAP];                      // staging (draw order), then positions: pad, draws, sentinels
@@ -538,10 +541,12 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
     RS_TS(tf1);
     RS_ACC(3, tf0, tf1);
     const u32 p0 = E * lane;
-#if RS_WL_SMEMST
-    // reloaded here (not live in registers through the count/scatter/sort)
-    base = sh.cur_base;
-    dst = reinterpret_cast<u64 *>(sh.cur_dst);
+#if RS_WL_SMEMST || RS_WL_SMEMST_GR
+    if (RS_WL_SMEMST || GR) {
+        // reloaded here (not live in registers through the count/scatter/sort)
+        base = sh.cur_base;
+        dst = reinterpret_cast<u64 *>(sh.cur_dst);
+    }
 #endif
     u64 *d0 = dst - h;                           // 32-byte aligned
     if (!WR) {
@@ -687,10 +692,13 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
         const u32 h = (u32)(reinterpret_cast<uintptr_t>(dst) >> 3) & 3u;
         const int shb = cr > WL_LOGB ? cr - WL_LOGB : 0;
         const u64 base = g.lo + 1;
-#if RS_WL_SMEMST
-        if (lane == 0) { sh.cur_base = base; sh.cur_dst = reinterpret_cast<unsigned long long>(dst); }
-        __syncwarp();
+#if RS_WL_SMEMST || RS_WL_SMEMST_GR
+        if (RS_WL_SMEMST || GR) {
+            if (lane == 0) { sh.cur_base = base; sh.cur_dst = reinterpret_cast<unsigned long long>(dst); }
+            __syncwarp();
+        }
 #endif
+        constexpr bool SMST = RS_WL_SMEMST || (RS_WL_SMEMST_GR && GR);
         u32 J = k;
         for (;;) {
             u32 res = 0xffffffffu;
@@ -704,7 +712,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
                     wl_scatter(sh, a.rk, dr, J, h, shb, lane);
                     RS_TS(ts1);
                     RS_ACC(2, ts0, ts1);
-                    res = wl_finish<WL_E1, WR, GR, TU>(sh, J, k, h, P, RS_WL_SMEMST ? 0 : base, RS_WL_SMEMST ? nullptr : dst, lane, a.gV);
+                    res = wl_finish<WL_E1, WR, GR, TU>(sh, J, k, h, P, SMST ? 0 : base, SMST ? nullptr : dst, lane, a.gV);
                     RS_TS(ts2);
                     RS_ACC(5, ts1, ts2);
                 } else {
