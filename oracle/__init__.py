@@ -50,6 +50,7 @@ def lib():
             "rso_philox": (None, [P32, P32, P32]),
             "rso_u52": (dbl, [u32, u32]),
             "rso_draw": (u64, [u64, u32, u64, u64, u64]),
+            "rso_lemire64_scan": (None, [u64, u64, u64, u64, P64]),
             "rso_log": (dbl, [dbl]),
             "rso_log1p": (dbl, [dbl]),
             "rso_stirlerr": (dbl, [dbl]),
@@ -81,6 +82,7 @@ def lib():
             "rso_small_samples": (None, [u64, u64, u64, u64, i32, P64]),
             "rso_digest_leaves_replay": (i32, [u64, u64, u64, i32, i32, u64, u64, P64, P64]),
             "rso_bern_chunks_digest": (i32, [u64, dbl, u64, u64, u64, P64, P64]),
+            "rso_bern_chunks_digest_mt": (i32, [u64, dbl, u64, i32, u64, u64, P64, P64]),
             "rso_uneven_counts": (i32, [i32, P64, u64, u64, P64]),
             "rso_uneven_seed": (u64, [u64, u64]),
             "rso_edges": (None, [u64, P64, u64, P64]),
@@ -293,6 +295,22 @@ def bern_chunks_digest(N, rho, seed, c_lo, c_hi):
     d, v = C.c_uint64(), C.c_uint64()
     _check(lib().rso_bern_chunks_digest(N, rho, seed, c_lo, c_hi, C.byref(d), C.byref(v)))
     return d.value, v.value
+
+
+def bern_digest(N, rho, seed, c_lo=0, c_hi=2**64 - 1, nthreads=None):
+    """(digest, count) of Bernoulli chunks [c_lo, c_hi) with threads (digest
+    indices start at 0 for chunk c_lo)."""
+    nthreads = nthreads or os.cpu_count() or 1
+    d, v = C.c_uint64(), C.c_uint64()
+    _check(lib().rso_bern_chunks_digest_mt(N, rho, seed, nthreads, c_lo, c_hi, C.byref(d), C.byref(v)))
+    return d.value, v.value
+
+
+def lemire64_scan(r, v, w_lo, w_hi):
+    """Test hook: (#accepted words -> v, #accepted -> other, #rejected) over [w_lo, w_hi)."""
+    o = np.zeros(3, dtype=np.uint64)
+    lib().rso_lemire64_scan(r, v, w_lo, w_hi, _p64(o))
+    return tuple(int(x) for x in o)
 
 
 def uneven_counts(L, n, seed):

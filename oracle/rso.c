@@ -115,6 +115,18 @@ int rso_lemire32(u32 word, u64 r, u64 *value)
     return (prod & 0xffffffffull) >= thresh;
 }
 
+/* Lemire's map of one 64-bit word to [0, r), 2^32 < r < 2^64: accept iff the
+ * low half of the 128-bit product word*r is >= 2^64 mod r; value = high half
+ * (the r > 2^32 branch of CANON C3; pinned by preimage counting:
+ * tests/test_oracle_primitives.py::test_lemire64_preimages). */
+int rso_lemire64(u64 word, u64 r, u64 *value)
+{
+    u64 thresh = (u64)(((u128)1 << 64) % r); /* 2^64 mod r */
+    u128 prod = (u128)word * r;
+    *value = (u64)(prod >> 64);
+    return (u64)prod >= thresh;
+}
+
 u64 rso_draw(u64 seed, u32 purpose, u64 id, u64 r, u64 j)
 {
     u32 w[4];
@@ -127,9 +139,8 @@ u64 rso_draw(u64 seed, u32 purpose, u64 id, u64 r, u64 j)
             if (rso_lemire32(word, r, &v)) return v;
         }
     } else {
-        u64 thresh = (u64)(((u128)1 << 64) % r); /* 2^64 mod r */
         for (u32 a = 0;; a++) {
-            u64 word;
+            u64 word, v;
             if (a == 0) {
                 block(seed, purpose, 0, id, (u32)(j >> 1), w);
                 word = (j & 1) ? (((u64)w[2] << 32) | w[3]) : (((u64)w[0] << 32) | w[1]);
@@ -137,8 +148,7 @@ u64 rso_draw(u64 seed, u32 purpose, u64 id, u64 r, u64 j)
                 block(seed, purpose, a, id, (u32)j, w);
                 word = ((u64)w[0] << 32) | w[1];
             }
-            u128 prod = (u128)word * r;
-            if ((u64)prod >= thresh) return (u64)(prod >> 64);
+            if (rso_lemire64(word, r, &v)) return v;
         }
     }
 }
@@ -847,6 +857,20 @@ u64 rso_lemire32_hist(u64 r, u32 *hist)
     return acc;
 }
 
+/* Every word w in [w_lo, w_hi) through rso_lemire64: out[0] = accepted words
+ * whose value is v, out[1] = accepted words with any other value, out[2] =
+ * rejected words.  The caller computes the preimage interval of v with exact
+ * integers (tests/test_oracle_primitives.py). */
+void rso_lemire64_scan(u64 r, u64 v, u64 w_lo, u64 w_hi, u64 out[3])
+{
+    out[0] = out[1] = out[2] = 0;
+    for (u64 w = w_lo; w != w_hi; w++) {
+        u64 x;
+        if (rso_lemire64(w, r, &x)) { if (x == v) out[0]++; else out[1]++; }
+        else out[2]++;
+    }
+}
+
 /* count deviates with node ids id0, id0+1, ... */
 void rso_hgd_batch(u64 k, u64 L, u64 R, u64 seed, u64 id0, u64 count, u64 *out)
 {
@@ -953,6 +977,72 @@ int rso_bern_chunks_digest(u64 N, double rho, u64 seed, u64 c_lo, u64 c_hi, u64 
     }
     free(buf);
     *digest = dig; *values = vals;
+    return RSO_OK;
+}
+
+/* The same over chunks [c_lo, c_hi) with nthreads workers, in two passes
+ * (counts, then digests at the prefix offsets): the whole-output parity of
+ * the roofline-sized Bernoulli run.  Threads only split independent chunks;
+ * each chunk is bern_chunk above. */
+typedef struct {
+    u64 N, seed; int Db; double lr;
+    u64 c_lo, c_hi, next; pthread_mutex_t mu;
+    u64 *cnt;                 /* per-chunk counts (pass 1) / offsets (pass 2) */
+    int pass; u64 digest;
+} bjob_t;
+
+static void *bworker(void *arg)
+{
+    bjob_t *J = (bjob_t *)arg;
+    u64 *buf = NULL, cap = 0, dig = 0;
+    for (;;) {
+        pthread_mutex_lock(&J->mu);
+        u64 i0 = J->next; J->next += 64;
+        pthread_mutex_unlock(&J->mu);
+        if (i0 >= J->c_hi) break;
+        for (u64 i = i0; i < i0 + 64 && i < J->c_hi; i++) {
+            if (J->pass == 1) { J->cnt[i - J->c_lo] = bern_chunk(J->N, J->seed, J->Db, i, J->lr, NULL); continue; }
+            u64 c = bern_chunk(J->N, J->seed, J->Db, i, J->lr, NULL);
+            if (c + 1 > cap) { free(buf); cap = c + 1; buf = (u64 *)malloc(cap * sizeof(u64)); }
+            bern_chunk(J->N, J->seed, J->Db, i, J->lr, buf);
+            dig += rso_digest(buf, c, J->cnt[i - J->c_lo]);
+        }
+    }
+    free(buf);
+    pthread_mutex_lock(&J->mu); J->digest += dig; pthread_mutex_unlock(&J->mu);
+    return NULL;
+}
+
+int rso_bern_chunks_digest_mt(u64 N, double rho, u64 seed, int nthreads, u64 c_lo, u64 c_hi,
+                              u64 *digest, u64 *values)
+{
+    if (!(rho > 0.0 && rho < 1.0)) return RSO_EINVAL;
+    bjob_t J;
+    memset(&J, 0, sizeof J);
+    J.N = N; J.seed = seed; J.Db = rso_bern_depth(N, rho); J.lr = rso_log1p(-rho);
+    u64 nch = (u64)1 << J.Db;
+    J.c_lo = c_lo < nch ? c_lo : nch;
+    J.c_hi = c_hi < nch ? c_hi : nch;
+    if (J.c_hi < J.c_lo) J.c_hi = J.c_lo;
+    J.cnt = (u64 *)malloc((J.c_hi - J.c_lo + 1) * sizeof(u64));
+    if (!J.cnt) return RSO_ENOMEM;
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_mutex_init(&J.mu, NULL);
+    pthread_t th[256];
+    for (J.pass = 1; J.pass <= 2; J.pass++) {
+        J.next = J.c_lo;
+        for (int t = 0; t < nthreads; t++) pthread_create(&th[t], NULL, bworker, &J);
+        for (int t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
+        if (J.pass == 1) {                  /* exclusive prefix: offsets */
+            u64 acc = 0;
+            for (u64 i = 0; i < J.c_hi - J.c_lo; i++) { u64 c = J.cnt[i]; J.cnt[i] = acc; acc += c; }
+            *values = acc;
+        }
+    }
+    pthread_mutex_destroy(&J.mu);
+    free(J.cnt);
+    *digest = J.digest;
     return RSO_OK;
 }
 

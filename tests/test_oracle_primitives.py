@@ -76,6 +76,34 @@ def test_lemire_power_of_two_is_shift():
             assert ok == 1 and v.value == w >> (32 - s)
 
 
+def _ceil_div(a, b):
+    return -(-a // b)
+
+
+@pytest.mark.parametrize("r", [(1 << 38) + 1, 3 * (1 << 37) + 12345, (1 << 40) - 3,
+                               (1 << 44) + 777, (1 << 62) + 5, (1 << 63) - 25])
+def test_lemire64_preimages(r):
+    """CANON C3, r > 2^32 branch (rso_lemire64, used by rso_draw): value v's
+    preimage words are exactly w in [ceil(v 2^64 / r), ceil((v+1) 2^64 / r))
+    (floor(w r / 2^64) = v, exact integer arithmetic here), and of those exactly
+    floor(2^64 / r) must be accepted -- the same count for every v, i.e. no
+    modulo bias.  A reversed accept test or a wrong threshold changes
+    the count for some v.  The words just outside the interval must not
+    produce v."""
+    q = (1 << 64) // r
+    rng = random.Random(r)
+    vs = {0, 1, r - 1, r // 2} | {rng.randrange(r) for _ in range(3)}
+    for v in sorted(vs):
+        lo = _ceil_div(v << 64, r)
+        hi = min(_ceil_div((v + 1) << 64, r), 1 << 64)
+        acc, other, rej = O.lemire64_scan(r, v, lo, hi)
+        assert other == 0 and acc == q and acc + rej == hi - lo, (r, v, acc, other, rej)
+        if lo > 0:
+            assert O.lemire64_scan(r, v, lo - 1, lo)[0] == 0
+        if hi < (1 << 64):
+            assert O.lemire64_scan(r, v, hi, hi + 1)[0] == 0
+
+
 def test_draw_in_range_and_64bit_path():
     for r in (1, 2, 7, 1 << 26, (1 << 32) - 1, 1 << 32, (1 << 32) + 1, 3 << 40, (1 << 62) + 5):
         for j in range(64):
