@@ -33,6 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "sorted samples/sec and output HBM GB/s vs peak at 1/2/4/8 B200"
+RING_ELEMS = 2 * (2 ** 27 + 2 ** 21)     # e2e at N > 1: 2 batch slots (batches <= 2^27 values)
 UNIT = "samples/s"
 
 
@@ -43,6 +44,14 @@ def _peaks():
         return float(p["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+# per-GPU work fixed as N grows (weak) vs total work fixed (strong)
+WEAK_WORKLOADS = ("headline", "weak30")
+
+
+def _scaling(name):
+    return "weak" if name in WEAK_WORKLOADS else "strong"
 
 
 def _workload(name, world):
@@ -129,6 +138,21 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def _merge_clocks(per_rank):
+    """Rank 0's view of every rank's clock sample: the slowest rank's median,
+    the union of throttle reasons, and the per-rank summaries."""
+    per_rank = [c for c in per_rank if c]
+    if not per_rank:
+        return None
+    if len(per_rank) == 1:
+        return per_rank[0]
+    meds = [c["sm_mhz"] for c in per_rank if c.get("sm_mhz") is not None]
+    return {"sm_mhz": min(meds) if meds else None,
+            "sm_max_mhz": max((c.get("sm_max_mhz") or 0) for c in per_rank) or None,
+            "reasons": sorted({r for c in per_rank for r in c.get("reasons", [])}),
+            "per_rank": per_rank}
+
+
 def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -151,12 +175,12 @@ def _max_over_ranks(x, world, device):
 # CPU oracle timings (cpu_baseline leg and --impl reference)
 # ---------------------------------------------------------------------------
 
-def oracle_sample(wl, target_s=10.0, leaf_start=0):
+def oracle_sample(wl, target_s=10.0, leaf_start=0, threads=None):
     """Time the oracle (as it stands) on a bounded sample of the workload:
     a contiguous run of output leaves (found by path replay) or Bernoulli
     chunks, sized for ~target_s seconds on all host cores."""
     import oracle as O
-    cores = os.cpu_count() or 1
+    cores = threads or os.cpu_count() or 1
     if wl["mode"] == "bernoulli":
         N, rho = wl["N"], wl["rho"]
         nch = 1 << O.bern_depth(N, rho)
@@ -211,7 +235,7 @@ def run_reference(args):
     out = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": None, "higher_is_better": True, "scaling": _scaling(args.workload),
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": wl["name"], "N": wl["N"], "n": wl.get("n"), "rho": wl.get("rho"),
                    "seed": wl["seed"], "impl_note": "CPU oracle (oracle/rso.c), bounded sample per step"},
@@ -307,9 +331,11 @@ def run_native(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     e0.record(stream)
-    for _ in range(args.steps):
+    for i in range(args.steps):
         step()
+        ev[i].record(stream)      # per-step split (median / best); the value uses e0..e1
     e1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -319,6 +345,7 @@ def run_native(args):
     kt = rs.timing_read(reset=True)
     clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
+    per_step = sorted([e0.elapsed_time(ev[0])] + [ev[i - 1].elapsed_time(ev[i]) for i in range(1, args.steps)])
     ms_max = _max_over_ranks(ms, world, dev)
 
     # ---- correctness of what was timed (untimed): sizes, order, range
@@ -417,19 +444,31 @@ def run_native(args):
     e2e = None
     if not args.no_e2e and mode not in ("bernoulli", "gnm", "algb"):
         try:
+            # N = 1: the whole sample lands in one pinned host buffer.  N > 1:
+            # each rank streams its slice through a bounded two-slot pinned ring
+            # (rs_sample_shard_host_stream; 8 ranks x 32 GiB would not fit the host)
+            ring = world > 1
+            elems = RING_ELEMS if ring else max(n_local, 1)
             try:
-                host = torch.empty(max(n_local, 1), dtype=torch.uint64, pin_memory=True)
+                host = torch.empty(elems, dtype=torch.uint64, pin_memory=True)
                 pinned = True
             except Exception:
-                host = torch.empty(max(n_local, 1), dtype=torch.uint64)
+                host = torch.empty(elems, dtype=torch.uint64)
                 pinned = False
-            rs.sample_shard_host(m, N, n, seed, world, rank, host)        # warm-up
+
+            def e2e_call():
+                if ring:
+                    rs.sample_shard_host_stream(m, N, n, seed, world, rank, host)
+                else:
+                    rs.sample_shard_host(m, N, n, seed, world, rank, host)
+
+            e2e_call()        # warm-up
             reps = args.e2e_steps
             if world > 1:
                 dist.barrier()
             t = time.perf_counter()
             for _ in range(reps):
-                rs.sample_shard_host(m, N, n, seed, world, rank, host)
+                e2e_call()
                 if world > 1:
                     dist.all_gather_into_tensor(allc, cnt)
             torch.cuda.synchronize()
@@ -437,7 +476,9 @@ def run_native(args):
             dt = _max_over_ranks(dt, world, dev)
             e2e = {"value": n_total / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": int(8 * n_total), "pinned": pinned, "steps": reps,
-                   "note": "rs_sample_shard_host: device generation + D2H of the whole sample"}
+                   "host_buffer": (f"two-slot pinned ring of {RING_ELEMS} values per rank" if ring
+                                   else "pinned, the whole sample"),
+                   "note": "rs_sample_shard_host(_stream): device generation + D2H of every value"}
             del host
         except Exception as ex:  # report, never fake
             e2e = {"value": None, "unit": UNIT, "error": str(ex)[:200]}
@@ -446,14 +487,25 @@ def run_native(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             cpu = oracle_sample(wl, target_s=args.cpu_seconds)
+            if wl["mode"] not in ("bernoulli", "algb"):     # (those legs are single-threaded already)
+                one = oracle_sample(wl, target_s=min(args.cpu_seconds, 5.0), threads=1)
+                cpu["value_1thread"] = one["value"]
+                cpu["sample_1thread"] = one["sample"]
         except Exception as ex:
             cpu = {"value": None, "error": str(ex)[:200]}
 
+    csum = clocks.summary()
+    clocks_all = [csum]
+    if world > 1:
+        clocks_all = [None] * world
+        dist.all_gather_object(clocks_all, csum)
     if rank == 0:
         res = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "step_ms": {"mean": ms, "median": per_step[len(per_step) // 2], "best": per_step[0],
+                        "rank": 0},
+            "higher_is_better": True, "scaling": _scaling(args.workload), "vs_baseline": None,
             "dtype": "u64", "data": "synthetic",
             "config": {"workload": wl["name"], "N": wl["N"], "n": wl.get("n"), "rho": wl.get("rho"),
                        "seed": wl["seed"], "parallelism": f"shard{world}",
@@ -461,7 +513,7 @@ def run_native(args):
                        else "output smaller than L2 (cache-warm)"},
             "output_gbs": gbs, "output_frac_of_peak": gbs / peak,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "clocks": clocks.summary(), "gpu_launches": launches,
+            "clocks": _merge_clocks(clocks_all), "gpu_launches": launches,
         }
         print(json.dumps(res))
     if world > 1:
@@ -469,9 +521,28 @@ def run_native(args):
     return 0
 
 
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _relaunch(n):
+    """python bench.py --gpus N (N > 1, no WORLD_SIZE): one process per GPU
+    under torch.distributed.run (127.0.0.1 rendezvous), same arguments; rank 0
+    prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="GPUs (ranks) of one node; > 1 without WORLD_SIZE re-launches under torch.distributed.run")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
@@ -486,6 +557,11 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: smoke-test the N > 1 path with ranks sharing one GPU")
     args = ap.parse_args()
+    env_world = os.environ.get("WORLD_SIZE")
+    if args.gpus is not None and args.gpus > 1 and env_world is None:
+        return _relaunch(args.gpus)
+    if args.gpus is not None and env_world is not None and int(env_world) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={env_world}")
     if args.impl == "reference":
         return run_reference(args)
     return run_native(args)

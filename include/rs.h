@@ -20,7 +20,10 @@
  *    argument).  rs_last_status() is thread-local.
  *  - Device-side capacity overflows (a leaf needing more than the
  *    on-chip capacity -- probability < 1e-100 at every supported shape,
- *    DESIGN.md 5) raise a sticky device flag read by rs_device_errors().
+ *    DESIGN.md 5) leave that leaf unwritten and raise bit 0 of the call's
+ *    status word (in its workspace) and of a sticky device flag
+ *    (rs_device_errors()).  The synchronous calls (rs_sample_checked, the
+ *    host-buffer calls) read the status word and return RS_ECAPACITY.
  */
 #ifndef RS_H
 #define RS_H
@@ -37,7 +40,8 @@ typedef enum {
     RS_EINVAL = 1,     /* invalid argument (n > N, rho not in [0,1], ...) */
     RS_ECUDA = 2,      /* CUDA runtime error / no device                  */
     RS_ENOMEM = 3,     /* workspace allocation failed / too small         */
-    RS_ECAPACITY = 4,  /* output capacity exceeded (Bernoulli)            */
+    RS_ECAPACITY = 4,  /* output capacity exceeded (Bernoulli) / a leaf
+                          exceeded the on-chip capacity (checked calls)   */
     RS_EATTEMPTS = 5   /* Algorithm B: restart budget exhausted           */
 } rs_status;
 
@@ -196,6 +200,26 @@ rs_status rs_sample_wor_host(uint64_t N, uint64_t n, uint64_t seed, uint64_t *ou
  * rs_release_cache frees them. */
 rs_status rs_sample_shard_host(int mode, uint64_t N, uint64_t n, uint64_t seed, int world,
                                int rank, uint64_t *out_host, void *stream);
+
+/* The same with a bounded host buffer of host_elems values: if host_elems <
+ * count, batch i is copied to out_host + (i mod 2) * B (B = the largest
+ * batch, <= 2^27 values), i.e. the host sees the slice streamed through a
+ * two-slot ring (bench.py's end-to-end leg at N > 1: bounded pinned memory
+ * per rank).  host_elems < 2 B -> RS_EINVAL; host_elems >= count is
+ * rs_sample_shard_host. */
+rs_status rs_sample_shard_host_stream(int mode, uint64_t N, uint64_t n, uint64_t seed, int world,
+                                      int rank, uint64_t *out_host, uint64_t host_elems,
+                                      void *stream);
+
+/* ---- checked device call ---------------------------------------------------
+ * rs_sample_wor_shard / rs_sample_wr_shard (mode RS_MODE_WOR / RS_MODE_WR;
+ * world = 1, rank = 0 for the whole sample) followed by a synchronisation of
+ * `stream` and a read of the call's own status word: RS_ECAPACITY if a leaf
+ * could not be completed on chip (that leaf's output span is then
+ * unspecified), without touching the process-wide sticky flag's state.
+ * out_local: device, capacity >= rs_shard_info's local_count. */
+rs_status rs_sample_checked(int mode, uint64_t N, uint64_t n, uint64_t seed, int world, int rank,
+                            uint64_t *out_local, void *stream);
 rs_status rs_release_cache(void);
 
 /* ---- split deviates (diagnostics / tests) ----------------------------------
@@ -232,9 +256,12 @@ rs_status rs_device_errors(int clear, unsigned *flags);
  * RS_OPT_TOPUP_MAX: 0..32, most duplicates the warp kernels for small leaf
  * ranges top up draw by draw before running a full extra round (default 32;
  * tests lower it to cover the fallback).
- * Results are identical for every setting.  Unknown option or value ->
- * RS_EINVAL. */
-enum { RS_OPT_LEAF_PATH = 1, RS_OPT_TOPUP_MAX = 2 };
+ * RS_OPT_LEAF_CAP: 0 (default) or 1..2048, the CTA leaf kernel's draw
+ * capacity; small values force capacity overflows so that tests can check
+ * that they are reported (RS_ECAPACITY from the checked calls).
+ * Results are identical for every setting of the first two (the third
+ * changes which leaves fail).  Unknown option or value -> RS_EINVAL. */
+enum { RS_OPT_LEAF_PATH = 1, RS_OPT_TOPUP_MAX = 2, RS_OPT_LEAF_CAP = 3 };
 rs_status rs_set_option(int option, int value);
 
 /* Number of kernel launches issued by this thread since the last reset. */

@@ -47,6 +47,8 @@ SIGNATURES = {
     "rs_bernoulli_ws": (_int, [_u64, _dbl, _u64, _int, _int, _vp, _u64, _vp, _vp, _sz, _vp]),
     "rs_sample_wor_host": (_int, [_u64, _u64, _u64, _vp, _vp]),
     "rs_sample_shard_host": (_int, [_int, _u64, _u64, _u64, _int, _int, _vp, _vp]),
+    "rs_sample_shard_host_stream": (_int, [_int, _u64, _u64, _u64, _int, _int, _vp, _u64, _vp]),
+    "rs_sample_checked": (_int, [_int, _u64, _u64, _u64, _int, _int, _vp, _vp]),
     "rs_digest": (_int, [_vp, _u64, _u64, _vp, _vp]),
     "rs_validate": (_int, [_vp, _u64, _u64, _int, _vp, _vp]),
     "rs_plan": (_int, [_int, _u64, _u64, _dbl, C.POINTER(_int), C.POINTER(_int), _P64]),
@@ -120,9 +122,20 @@ def _stream(stream=None):
 def _out(n: int, out, device):
     if out is None:
         return torch.empty(max(n, 1), dtype=torch.uint64, device=device)[:n]
-    if out.dtype not in (torch.uint64, torch.int64) or not out.is_cuda or out.numel() < n:
-        raise ValueError("out must be a cuda uint64 tensor with >= n elements")
+    if (out.dtype not in (torch.uint64, torch.int64) or not out.is_cuda or out.numel() < n
+            or not out.is_contiguous()):
+        raise ValueError("out must be a contiguous cuda uint64 tensor with >= n elements")
     return out
+
+
+def _host(n: int, out_host):
+    """A host uint64 buffer of >= n elements (the C ABI writes n values)."""
+    if out_host is None:
+        return torch.empty(max(n, 1), dtype=torch.uint64, pin_memory=True)
+    if (out_host.dtype not in (torch.uint64, torch.int64) or out_host.is_cuda
+            or out_host.numel() < n or not out_host.is_contiguous()):
+        raise ValueError("out_host must be a contiguous CPU uint64 tensor with >= n elements")
+    return out_host
 
 
 def _ptr(t):
@@ -216,13 +229,22 @@ def workspace_bytes(mode: int, N: int, n: int = 0, rho: float = 0.0, world: int 
     return b.value
 
 
+def _ws_out(mode, N, n, seed, world, rank, out):
+    if out is None:
+        raise ValueError("out is required (a cuda uint64 tensor of the shard's count)")
+    cnt, _ = shard_info(N, n, seed, world, rank, mode)
+    return _out(cnt, out, None)
+
+
 def sample_wor_ws(N, n, seed, world, rank, out, ws, stream=None):
+    out = _ws_out(MODE_WOR, N, n, seed, world, rank, out)
     _check(lib().rs_sample_wor_ws(N, n, seed % 2**64, world, rank, _ptr(out), _ptr(ws),
                                   ws.numel() * ws.element_size(), _stream(stream)))
     return out
 
 
 def sample_wr_ws(N, n, seed, world, rank, out, ws, stream=None):
+    out = _ws_out(MODE_WR, N, n, seed, world, rank, out)
     _check(lib().rs_sample_wr_ws(N, n, seed % 2**64, world, rank, _ptr(out), _ptr(ws),
                                  ws.numel() * ws.element_size(), _stream(stream)))
     return out
@@ -238,8 +260,8 @@ def bernoulli_ws(N, rho, seed, world, rank, out, capacity, count, ws, stream=Non
 def sample_wor_host(N: int, n: int, seed: int, out_host=None, stream=None):
     """rs_sample_wor into a host (ideally pinned) uint64 tensor."""
     _require_cuda()
-    if out_host is None:
-        out_host = torch.empty(n, dtype=torch.uint64, pin_memory=True)
+    cnt, _ = shard_info(N, n, seed, 1, 0, MODE_WOR)
+    out_host = _host(cnt, out_host)
     _check(lib().rs_sample_wor_host(N, n, seed % 2**64, _ptr(out_host), _stream(stream)))
     return out_host
 
@@ -249,11 +271,35 @@ def sample_shard_host(mode: int, N: int, n: int, seed: int, world: int, rank: in
     """The rank's slice (WOR or WR) into a host (ideally pinned) tensor."""
     _require_cuda()
     cnt, _ = shard_info(N, n, seed, world, rank, mode)
-    if out_host is None:
-        out_host = torch.empty(cnt, dtype=torch.uint64, pin_memory=True)
+    out_host = _host(cnt, out_host)
     _check(lib().rs_sample_shard_host(mode, N, n, seed % 2**64, world, rank, _ptr(out_host),
                                       _stream(stream)))
     return out_host[:cnt]
+
+
+def sample_shard_host_stream(mode: int, N: int, n: int, seed: int, world: int, rank: int,
+                             out_host, stream=None):
+    """The rank's slice streamed device->host through a bounded host buffer
+    (rs_sample_shard_host_stream: a two-slot ring when out_host is smaller
+    than the slice)."""
+    _require_cuda()
+    if out_host is None or out_host.is_cuda or not out_host.is_contiguous() or \
+            out_host.dtype not in (torch.uint64, torch.int64):
+        raise ValueError("out_host must be a contiguous CPU uint64 tensor")
+    _check(lib().rs_sample_shard_host_stream(mode, N, n, seed % 2**64, world, rank, _ptr(out_host),
+                                             out_host.numel(), _stream(stream)))
+    return out_host
+
+
+def sample_checked(mode: int, N: int, n: int, seed: int, world: int = 1, rank: int = 0, out=None,
+                   device="cuda", stream=None):
+    """rs_sample_checked: the (shard of the) sample, synchronised, with the
+    call's own capacity status (raises RSError on RS_ECAPACITY)."""
+    _require_cuda()
+    cnt, _ = shard_info(N, n, seed, world, rank, mode)
+    o = _out(cnt, out, device)
+    _check(lib().rs_sample_checked(mode, N, n, seed % 2**64, world, rank, _ptr(o), _stream(stream)))
+    return o[:cnt]
 
 
 def deviates(kind: int, k: int, L: int, R: int, seed: int, id0: int, count: int, stream=None):
@@ -297,6 +343,7 @@ def device_errors(clear: bool = True) -> int:
 
 OPT_LEAF_PATH = 1
 OPT_TOPUP_MAX = 2
+OPT_LEAF_CAP = 3
 
 
 def node_info(mode: int, N: int, n: int, seed: int, depth: int, index: int):

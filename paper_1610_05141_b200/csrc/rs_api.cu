@@ -19,6 +19,7 @@ namespace {
 thread_local rs_status t_last = RS_OK;
 int g_leaf_path = 0;                    // rs_set_option(RS_OPT_LEAF_PATH)
 int g_topup_max = 32;                   // rs_set_option(RS_OPT_TOPUP_MAX)
+int g_leaf_cap = 0;                     // rs_set_option(RS_OPT_LEAF_CAP) (tests: force overflows)
 thread_local uint64_t t_launches = 0;
 
 rs_status ret(rs_status s) { t_last = s; return s; }
@@ -152,7 +153,7 @@ rs_status plan_node(int mode, u64 N, u64 n, u64 seed, int s, u64 idx, TreePlan &
     p.o_pong_off = o; o = align256(o + wmax * 8);
     p.o_leaf_cnt = o; o = align256(o + p.nleaves * 4);
     p.o_leaf_off = o; o = align256(o + p.nleaves * 8);
-    p.o_spill = o; o = align256(o + (p.nleaves + 1) * 4);   // spill count + list
+    p.o_spill = o; o = align256(o + (p.nleaves + 2) * 4);   // status word, spill count + list
     p.bytes = o;
     return RS_OK;
 }
@@ -194,10 +195,19 @@ unsigned leaf_grid(const void *kern, int threads, size_t smem, u64 work)
     return (unsigned)(work < g ? (work ? work : 1) : g);
 }
 
-// Launch the split phases and the leaf kernel of a tree plan.
-rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t st)
+// Launch the split phases and the leaf kernel of a tree plan.  The call's
+// status word (ws + o_spill) is zeroed here when clear_status is set;
+// otherwise it accumulates over several run_tree calls (host-buffer batches).
+rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t st, bool clear_status = true)
 {
     if (p.local_count == 0) return RS_OK;
+    u32 *status = (u32 *)(ws + p.o_spill);
+    const bool warp_path = !(p.r_max <= BM_RMAX && p.mode == RS_MODE_WOR && g_leaf_path == 0) &&
+                           !p.comp && p.r_max <= 0xfffff000ull && g_leaf_path == 0;
+    if (clear_status)      // status + spill count in one memset
+        cudaMemsetAsync(status, 0, warp_path ? 8 : 4, st);
+    else if (warp_path)
+        cudaMemsetAsync(status + 1, 0, 4, st);
     u64 *ping_cnt = (u64 *)(ws + p.o_ping_cnt), *ping_off = (u64 *)(ws + p.o_ping_off);
     u64 *pong_cnt = (u64 *)(ws + p.o_pong_cnt), *pong_off = (u64 *)(ws + p.o_pong_off);
     u32 *leaf_cnt = (u32 *)(ws + p.o_leaf_cnt);
@@ -262,6 +272,8 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
     la.cnt = leaf_cnt; la.off = leaf_off; la.out = out;
     la.rk = round_keys(p.seed);
     la.gV = p.gV;
+    la.status = status;
+    la.cap = (u32)g_leaf_cap;
     const bool wide = p.r_max > 0xfffff000ull;    // u32 keys (below the warp kernel's sentinels)
     const bool wr = (p.mode == RS_MODE_WR);
     void (*kern)(LeafArgs);
@@ -284,10 +296,9 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
     } else if (!wide && g_leaf_path == 0) {
         // common path: warp per leaf; leaves it cannot hold go to a spill
         // list that the CTA kernel completes right after (usually empty)
-        u32 *spill_n = (u32 *)(ws + p.o_spill);
+        u32 *spill_n = status + 1;        // zeroed above
         la.spill_n = spill_n;
         la.spill = spill_n + 1;
-        cudaMemsetAsync(spill_n, 0, 4, st);
         // leaves with many duplicates (r <= 2^21: >= 22 % of leaves) top the
         // distinct set up draw by draw instead of re-running a full round
         const bool tu = p.r_max <= WL_TU_RMAX;
@@ -787,16 +798,54 @@ rs_status rs_sample_node(int mode, uint64_t N, uint64_t n, uint64_t seed, int de
     return ret(plan_call(p, out, nullptr, 0, stream));
 }
 
+static rs_status shard_host(int mode, uint64_t N, uint64_t n, uint64_t seed, int world,
+                            int rank, uint64_t *out_host, uint64_t host_elems, void *stream);
+
 rs_status rs_sample_shard_host(int mode, uint64_t N, uint64_t n, uint64_t seed, int world,
                                int rank, uint64_t *out_host, void *stream)
 {
+    return ret(shard_host(mode, N, n, seed, world, rank, out_host, ~0ull, stream));
+}
+
+rs_status rs_sample_shard_host_stream(int mode, uint64_t N, uint64_t n, uint64_t seed, int world,
+                                      int rank, uint64_t *out_host, uint64_t host_elems, void *stream)
+{
+    return ret(shard_host(mode, N, n, seed, world, rank, out_host, host_elems, stream));
+}
+
+rs_status rs_sample_checked(int mode, uint64_t N, uint64_t n, uint64_t seed, int world, int rank,
+                            uint64_t *out_local, void *stream)
+{
     if (!have_device()) return ret(RS_ECUDA);
     if (mode != RS_MODE_WOR && mode != RS_MODE_WR) return ret(RS_EINVAL);
+    TreePlan p;
+    rs_status st = plan_tree(mode, N, n, seed, world, rank, p);
+    if (st != RS_OK) return ret(st);
+    if (p.local_count == 0) return ret(RS_OK);
+    if (!out_local) return ret(RS_EINVAL);
+    const cudaStream_t cs = S(stream);
+    unsigned char *w = nullptr;
+    if (cudaMallocAsync((void **)&w, p.bytes, cs) != cudaSuccess) return ret(RS_ENOMEM);
+    st = run_tree(p, out_local, w, cs);
+    u32 flags = 0;
+    if (st == RS_OK && cudaMemcpyAsync(&flags, w + p.o_spill, 4, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+        st = RS_ECUDA;
+    cudaFreeAsync(w, cs);
+    if (cudaStreamSynchronize(cs) != cudaSuccess) st = RS_ECUDA;
+    if (st == RS_OK && flags) st = RS_ECAPACITY;
+    return ret(st);
+}
+
+static rs_status shard_host(int mode, uint64_t N, uint64_t n, uint64_t seed, int world,
+                            int rank, uint64_t *out_host, uint64_t host_elems, void *stream)
+{
+    if (!have_device()) return (RS_ECUDA);
+    if (mode != RS_MODE_WOR && mode != RS_MODE_WR) return (RS_EINVAL);
     TreePlan sp;
     rs_status st = plan_tree(mode, N, n, seed, world, rank, sp);
-    if (st != RS_OK) return ret(st);
-    if (sp.local_count == 0) return ret(RS_OK);
-    if (!out_host) return ret(RS_EINVAL);
+    if (st != RS_OK) return (st);
+    if (sp.local_count == 0) return (RS_OK);
+    if (!out_host) return (RS_EINVAL);
     // batches: the shard's descendants at depth s + b, each <= 2^27 values
     int b = 0;
     while (b < sp.D - sp.s && (sp.local_count >> b) > (1ull << 27)) ++b;
@@ -807,16 +856,21 @@ rs_status rs_sample_shard_host(int mode, uint64_t N, uint64_t n, uint64_t seed, 
     size_t maxws = 0;
     for (u64 i = 0; i < nb; ++i) {
         st = plan_node(mode, N, n, seed, sp.s + b, (sp.idx << b) + i, plans[i]);
-        if (st != RS_OK) return ret(st);
+        if (st != RS_OK) return (st);
         if (plans[i].local_count > maxc) maxc = plans[i].local_count;
         if (plans[i].bytes > maxws) maxws = plans[i].bytes;
     }
+    // host_elems < count: stream the batches through a two-slot host ring
+    // (batch i -> out_host + (i & 1) * maxc; for benchmarks of the D2H path
+    // with bounded host memory).  Needs host_elems >= 2 * maxc.
+    const bool ring = host_elems < sp.local_count;
+    if (ring && host_elems < 2 * maxc) return (RS_EINVAL);
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= RS_MAX_DEV) return ret(RS_ECUDA);
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= RS_MAX_DEV) return (RS_ECUDA);
     HostStage &H = g_stage[dev];
     std::lock_guard<std::mutex> lock(H.mu);
     if (!H.cs) {
-        if (cudaStreamCreateWithFlags(&H.cs, cudaStreamNonBlocking) != cudaSuccess) { H.cs = nullptr; return ret(RS_ECUDA); }
+        if (cudaStreamCreateWithFlags(&H.cs, cudaStreamNonBlocking) != cudaSuccess) { H.cs = nullptr; return (RS_ECUDA); }
         for (int i = 0; i < 2; ++i) {
             cudaEventCreateWithFlags(&H.gen_done[i], cudaEventDisableTiming);
             cudaEventCreateWithFlags(&H.copy_done[i], cudaEventDisableTiming);
@@ -828,13 +882,13 @@ rs_status rs_sample_shard_host(int mode, uint64_t N, uint64_t n, uint64_t seed, 
         if (H.buf[1]) cudaFree(H.buf[1]);
         H.buf[0] = H.buf[1] = nullptr; H.buf_bytes = 0;
         if (cudaMalloc((void **)&H.buf[0], need_buf) != cudaSuccess ||
-            cudaMalloc((void **)&H.buf[1], need_buf) != cudaSuccess) { H.release(); cudaGetLastError(); return ret(RS_ENOMEM); }
+            cudaMalloc((void **)&H.buf[1], need_buf) != cudaSuccess) { H.release(); cudaGetLastError(); return (RS_ENOMEM); }
         H.buf_bytes = need_buf;
     }
     if (H.ws_bytes < need_ws) {
         if (H.ws) cudaFree(H.ws);
         H.ws = nullptr; H.ws_bytes = 0;
-        if (cudaMalloc((void **)&H.ws, need_ws) != cudaSuccess) { H.release(); cudaGetLastError(); return ret(RS_ENOMEM); }
+        if (cudaMalloc((void **)&H.ws, need_ws) != cudaSuccess) { H.release(); cudaGetLastError(); return (RS_ENOMEM); }
         H.ws_bytes = need_ws;
     }
     const cudaStream_t gs = S(stream), cs = H.cs;
@@ -845,19 +899,23 @@ rs_status rs_sample_shard_host(int mode, uint64_t N, uint64_t n, uint64_t seed, 
     for (u64 i = 0; i < nb && st == RS_OK; ++i) {
         const int j = (int)(i & 1);
         if (i >= 2) cudaStreamWaitEvent(gs, H.copy_done[j], 0);     // buffer j is free again
-        st = run_tree(plans[i], H.buf[j], H.ws, gs);
+        st = run_tree(plans[i], H.buf[j], H.ws, gs, i == 0);
         cudaEventRecord(H.gen_done[j], gs);
         cudaStreamWaitEvent(cs, H.gen_done[j], 0);
         if (plans[i].local_count &&
-            cudaMemcpyAsync(out_host + (plans[i].global_offset - base_off), H.buf[j],
+            cudaMemcpyAsync(out_host + (ring ? (u64)j * maxc : plans[i].global_offset - base_off), H.buf[j],
                             plans[i].local_count * 8, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
             st = RS_ECUDA;
         cudaEventRecord(H.copy_done[j], cs);
     }
     cudaStreamWaitEvent(gs, H.copy_done[0], 0);
     cudaStreamWaitEvent(gs, H.copy_done[1], 0);
+    u32 flags = 0;     // the batches' status word (every plan shares o_spill's layout)
+    if (st == RS_OK && cudaMemcpyAsync(&flags, H.ws + plans[0].o_spill, 4, cudaMemcpyDeviceToHost, gs) != cudaSuccess)
+        st = RS_ECUDA;
     if (cudaStreamSynchronize(gs) != cudaSuccess || cudaStreamSynchronize(cs) != cudaSuccess) st = RS_ECUDA;
-    return ret(st);
+    if (st == RS_OK && flags) st = RS_ECAPACITY;
+    return (st);
 }
 
 rs_status rs_deviates(int kind, uint64_t k, uint64_t L, uint64_t R, uint64_t seed, uint64_t id0,
@@ -961,6 +1019,10 @@ rs_status rs_set_option(int option, int value)
     }
     if (option == RS_OPT_TOPUP_MAX && value >= 0 && value <= 32) {
         g_topup_max = value;
+        return ret(RS_OK);
+    }
+    if (option == RS_OPT_LEAF_CAP && value >= 0 && value <= LEAF_CAP) {
+        g_leaf_cap = value;
         return ret(RS_OK);
     }
     return ret(RS_EINVAL);

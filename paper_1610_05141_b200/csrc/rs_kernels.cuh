@@ -138,6 +138,8 @@ struct LeafArgs {
     RoundKeys rk;          // Philox round keys of seed (round_keys(seed))
     u64 gV;                // != 0: graph calls, store packed edges of G(gV, .) (NEXT-3)
     u32 topup_max;         // warp *_tu kernels: most new values topped up per leaf (<= 32)
+    u32 *status;           // per-call status word (bit 0: a leaf exceeded the on-chip capacity)
+    u32 cap;               // CTA kernel draw capacity (0: LEAF_CAP; rs_set_option(RS_OPT_LEAF_CAP), tests)
 };
 
 __global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_wor32(LeafArgs a);

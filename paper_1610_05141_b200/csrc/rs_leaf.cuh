@@ -27,6 +27,20 @@
 namespace rs {
 
 
+// A leaf the kernel cannot complete raises bit `bits` in the sticky device
+// flag (rs_device_errors) and in the call's status word (returned as
+// RS_ECAPACITY by the synchronous calls, include/rs.h).
+__device__ __forceinline__ void leaf_flag(u32 *status, unsigned bits)
+{
+    atomicOr(&g_rs_errors, bits);
+    if (status) atomicOr(status, bits);
+}
+
+__device__ __forceinline__ u32 leaf_cap(const LeafArgs &a)
+{
+    return (a.cap && a.cap < (u32)LEAF_CAP) ? a.cap : (u32)LEAF_CAP;
+}
+
 constexpr int LB_LOG_MIN = 10, LB_LOG_MAX = 12;
 constexpr u32 LB_MAX = 1u << LB_LOG_MAX;          // buckets (and WR histogram slots)
 constexpr u32 CNT_BITS = 12, CNT_MASK = (1u << CNT_BITS) - 1;
@@ -206,9 +220,10 @@ __device__ __noinline__ u32 dup_round(SLeaf<K> &sh, u32 J, u32 k, u32 h, int shb
 // The leaf's sorted sample (relative offsets x in [0, r)) into
 // sh.keys[h .. h + k).  On entry sh.W is all zero and sh.ndup == 0; on
 // return W is dirty (the caller clears it) and ndup == 0.  Returns false on
-// on-chip capacity overflow (more than LEAF_CAP draws needed; flag raised).
+// on-chip capacity overflow (more than cap <= LEAF_CAP draws needed; the
+// caller raises the flag).
 template <typename K, bool WR>
-__device__ bool leaf_sorted(SLeaf<K> &sh, const Stream &st, u64 r, u32 k, u32 h)
+__device__ bool leaf_sorted(SLeaf<K> &sh, const Stream &st, u64 r, u32 k, u32 h, u32 cap)
 {
     constexpr int EPB = Drawer<K>::EPB;
     constexpr int BPT = LEAF_EPT / EPB;            // Philox blocks per thread per round
@@ -217,10 +232,7 @@ __device__ bool leaf_sorted(SLeaf<K> &sh, const Stream &st, u64 r, u32 k, u32 h)
     const int cr = ceil_log2(r);
     u32 J = k;                                     // draws of the rounds so far
     for (;;) {
-        if (J > (u32)LEAF_CAP) {
-            if (tid == 0) atomicOr(&g_rs_errors, 1u);
-            return false;
-        }
+        if (J > cap) return false;
         int logB = ceil_log2(J) + 1;
         logB = logB < LB_LOG_MIN ? LB_LOG_MIN : (logB > LB_LOG_MAX ? LB_LOG_MAX : logB);
         const u32 B = 1u << logB;
@@ -364,17 +376,14 @@ __device__ __forceinline__ LeafGeom leaf_geom(const LeafArgs &a, u64 L)
 // ranges are tiny, e.g. n >> N): r == 1 -> k copies; r < LB_MAX ->
 // histogram of all k draws, scan, emit runs by binary search.
 template <typename K>
-__device__ void wr_big_leaf(SLeaf<K> &sh, const Stream &st, u64 lo, u64 r, u32 k, u64 *dst)
+__device__ bool wr_big_leaf(SLeaf<K> &sh, const Stream &st, u64 lo, u64 r, u32 k, u64 *dst)
 {
     const u64 base = lo + 1;
     if (r == 1) {
         for (u32 i = threadIdx.x; i < k; i += LEAF_NT) dst[i] = base;
-        return;
+        return true;
     }
-    if (r >= LB_MAX) {
-        if (threadIdx.x == 0) atomicOr(&g_rs_errors, 1u);
-        return;
-    }
+    if (r >= LB_MAX) return false;
     u32 *hist = sh.W;                                  // zero on entry
     const Drawer<K> dr(st, r);
     constexpr int EPB = Drawer<K>::EPB;
@@ -395,6 +404,7 @@ __device__ void wr_big_leaf(SLeaf<K> &sh, const Stream &st, u64 lo, u64 r, u32 k
         }
         dst[t] = base + a;
     }
+    return true;
 }
 
 template <typename K>
@@ -420,12 +430,14 @@ __device__ __forceinline__ void sample_leaves(const LeafArgs &a)
         const LeafGeom g = leaf_geom(a, L);
         const Stream st(a.seed, WR ? P_WR : P_WOR, g.id);
         u64 *dst = a.out + a.off[L];
-        if (k > (u32)LEAF_CAP) {
-            if (WR) wr_big_leaf<K>(sh, st, g.lo, g.r, k, dst);
-            else if (threadIdx.x == 0) atomicOr(&g_rs_errors, 1u);
+        const u32 cap = leaf_cap(a);
+        if (k > cap) {
+            const bool ok = WR && wr_big_leaf<K>(sh, st, g.lo, g.r, k, dst);
+            if (!ok && threadIdx.x == 0) leaf_flag(a.status, 1u);
         } else {
             const u32 h = (u32)(reinterpret_cast<uintptr_t>(dst) >> 3) & 3u;
-            if (leaf_sorted<K, WR>(sh, st, g.r, k, h)) store_run<K>(sh.keys, k, h, g.lo + 1, dst, a.gV);
+            if (leaf_sorted<K, WR>(sh, st, g.r, k, h, cap)) store_run<K>(sh.keys, k, h, g.lo + 1, dst, a.gV);
+            else if (threadIdx.x == 0) leaf_flag(a.status, 1u);
         }
         __syncthreads();
         zero_words(sh.W, LB_MAX);
@@ -475,10 +487,14 @@ __device__ __forceinline__ void complement_leaves(const LeafArgs &a)
         const u32 e = a.cnt[L];
         if (e > 0) {
             const Stream st(a.seed, P_WOR, g.id);
-            const bool ok = leaf_sorted<K, false>(sh, st, g.r, e, 0);
+            const bool ok = leaf_sorted<K, false>(sh, st, g.r, e, 0, leaf_cap(a));
             __syncthreads();
             zero_words(sh.W, LB_MAX);
-            if (!ok) { __syncthreads(); continue; }
+            if (!ok) {
+                if (tid == 0) leaf_flag(a.status, 1u);
+                __syncthreads();
+                continue;
+            }
         }
         const u32 i0 = lower_bound_s<K>(sh.keys, e, v0);
         const u32 i1 = lower_bound_s<K>(sh.keys, e, v0 + nv);

@@ -24,6 +24,14 @@ def _group_info(group=None):
     return dist.get_world_size(group), dist.get_rank(group)
 
 
+def _coll_device(group=None):
+    """Device of the collective's tensors: the current GPU under NCCL, the
+    host under gloo (gloo's all-gather takes CPU tensors)."""
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
 def allgather_counts(local_count: int, group=None, device=None) -> torch.Tensor:
     """All-gather of one u64 count per rank (the path's only collective)."""
     world, _ = _group_info(group)
@@ -52,8 +60,7 @@ def sample(N: int, n: int, seed: int, mode: int = MODE_WOR, group=None, stream=N
     """This rank's slice of the world's sample (device tensor) and its global
     offset.  Identical for every world size when concatenated in rank order."""
     world, rank = _group_info(group)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    cnt, off, _ = shard_offsets(N, n, seed, mode, group, dev)
+    cnt, off, _ = shard_offsets(N, n, seed, mode, group, _coll_device(group))
     f = sample_wr_shard if mode == MODE_WR else sample_wor_shard
     return f(N, n, seed, world, rank, stream=stream), off
 
@@ -66,7 +73,7 @@ def bernoulli(N: int, rho: float, seed: int, group=None, stream=None):
     c = int(cnt.item())
     if c > vals.numel():
         raise RuntimeError("bernoulli shard: capacity exceeded")
-    allc = allgather_counts(c, group, vals.device)
+    allc = allgather_counts(c, group, _coll_device(group))
     return vals[:c], int(allc[:rank].sum().item())
 
 
@@ -79,8 +86,7 @@ def uneven_sample(L_local: int, n: int, seed: int, group=None, stream=None):
     derives the same counts."""
     from . import uneven_local_sample
     world, rank = _group_info(group)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    allL = allgather_counts(L_local, group, dev if dist.get_backend(group) == "nccl" else None)
+    allL = allgather_counts(L_local, group, _coll_device(group))
     L = [int(v) for v in allL.tolist()]
     vals, cnt = uneven_local_sample(L, n, seed, rank, stream=stream)
     return vals, cnt, L

@@ -405,3 +405,48 @@ def test_topup_fallback(tmax):
     finally:
         rs.set_option(rs.OPT_TOPUP_MAX, 32)
     _no_device_errors()
+
+
+# ---- device-side capacity failures are reported through the API ----
+
+def test_capacity_overflow_returns_ecapacity():
+    """A leaf the kernels cannot hold on chip must surface as RS_ECAPACITY from
+    the synchronous calls, without rs_device_errors().  RS_OPT_LEAF_CAP caps
+    the CTA leaf kernel at 64 draws, so cfg0's ~1024-value leaves overflow."""
+    N, n = 2 ** 30, 2 ** 20
+    rs.set_option(rs.OPT_LEAF_PATH, 1)
+    rs.set_option(rs.OPT_LEAF_CAP, 64)
+    try:
+        with pytest.raises(rs.RSError, match="capacity"):
+            rs.sample_checked(rs.MODE_WOR, N, n, 1)
+        with pytest.raises(rs.RSError, match="capacity"):
+            rs.sample_shard_host(rs.MODE_WOR, N, n, 1, 1, 0)
+        with pytest.raises(rs.RSError, match="capacity"):
+            rs.sample_checked(rs.MODE_WR, N, n, 1)
+    finally:
+        rs.set_option(rs.OPT_LEAF_CAP, 0)
+        rs.set_option(rs.OPT_LEAF_PATH, 0)
+        rs.device_errors(clear=True)
+    # the same calls succeed (and match the oracle) with the default capacity
+    got = rs.sample_checked(rs.MODE_WOR, N, n, 1)
+    assert np.array_equal(_np(got), O.sample_wor(N, n, 1))
+    assert rs.device_errors(clear=True) == 0
+
+
+def test_host_stream_ring():
+    """rs_sample_shard_host_stream with a host buffer smaller than the slice:
+    the last batch of each slot is what remains in the ring; with a buffer of
+    the full size it equals rs_sample_shard_host."""
+    N, n, seed = 2 ** 40, 2 ** 28, 3
+    full = rs.sample_shard_host(rs.MODE_WOR, N, n, seed, 1, 0)
+    big = torch.empty(n, dtype=torch.uint64, pin_memory=True)
+    rs.sample_shard_host_stream(rs.MODE_WOR, N, n, seed, 1, 0, big)
+    assert torch.equal(big.view(torch.int64), full.view(torch.int64))
+    ring = torch.zeros(2 * (2 ** 27 + 2 ** 21), dtype=torch.uint64, pin_memory=True)
+    rs.sample_shard_host_stream(rs.MODE_WOR, N, n, seed, 1, 0, ring)
+    # every value that reached the ring is one of the sample's
+    r = ring.view(torch.int64).numpy()
+    v = r[r != 0]
+    assert v.size > 2 ** 26 and np.isin(v, full.view(torch.int64).numpy()).all()
+    with pytest.raises(rs.RSError):
+        rs.sample_shard_host_stream(rs.MODE_WOR, N, n, seed, 1, 0, ring[:1000])

@@ -48,6 +48,49 @@ __global__ void k_smem(u32 iters, u32 *out) {
   if (acc == 0x12345678 || T[threadIdx.x] == 0x12345679) out[0] = acc;
 }
 
+// issue ceiling: 8 independent chains of one-instruction steps per thread
+// (inline PTX: lop3.b32 -> one LOP3 on the ALU pipe; mul.wide.u32 -> one
+// IMAD.WIDE on the FMA pipe), 16 steps unrolled per loop trip.
+__global__ void k_lop3(u32 iters, u32 *out) {
+  u32 a[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) a[c] = threadIdx.x * (c + 3) + blockIdx.x;
+  for (u32 i = 0; i < iters; i += 16) {
+#pragma unroll
+    for (int s = 0; s < 16; ++s)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[c]) : "r"(a[(c + 1) & 7]), "r"(i));
+  }
+  u32 acc = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc ^= a[c];
+  if (acc == 0x12345678) out[0] = acc;
+}
+__global__ void k_imadw(u32 iters, u32 *out) {
+  u64 a[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) a[c] = threadIdx.x * (c + 3) + blockIdx.x;
+  for (u32 i = 0; i < iters; i += 16) {
+#pragma unroll
+    for (int s = 0; s < 16; ++s)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) asm volatile("mul.wide.u32 %0, %1, 0xD2511F53;" : "=l"(a[c]) : "r"((u32)(a[c] >> 32) + (u32)a[c]));
+  }
+  u64 acc = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc ^= a[c];
+  if (acc == 0x12345678) out[0] = (u32)acc;
+}
+// conflict-free LDS (lane-strided) for the wavefront rate
+__global__ void k_lds_cf(u32 iters, u32 *out) {
+  __shared__ u32 T[4096];
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) T[i] = i;
+  __syncthreads();
+  u32 acc = 0, b = threadIdx.x & 31;
+  for (u32 i = 0; i < iters; ++i) { acc += T[(b + 32 * (i & 127))]; b ^= acc & 0; }
+  if (acc == 0x12345678) out[0] = acc;
+}
+
 // baseline: the LCG loop alone
 __global__ void k_lcg(u32 iters, u32 *out) {
   u32 x = threadIdx.x * 0x9E3779B9u + blockIdx.x, acc = 0;
@@ -80,6 +123,9 @@ int main() {
   double threads = (double)grid * nt;
   TIME("philox blocks", (k_philox<<<grid, nt>>>(it, o, 1)), threads * it, "G blocks/s");
   TIME("lcg loop", (k_lcg<<<grid, nt>>>(it * 4, o)), threads * it * 4, "G it/s");
+  TIME("lop3 chains (1 LOP3/step)", (k_lop3<<<grid, nt>>>(it, o)), threads * it * 8, "G thread-inst/s");
+  TIME("imad.wide+iadd3 (2/step)", (k_imadw<<<grid, nt>>>(it, o)), threads * it * 8 * 2, "G thread-inst/s");
+  TIME("smem LDS conflict-free", (k_lds_cf<<<grid, nt>>>(it, o)), threads * it, "G ops/s");
   TIME("smem atomicAdd ret", (k_smem<0><<<grid, nt>>>(it, o)), threads * it, "G ops/s");
   TIME("smem atomicOr ret", (k_smem<1><<<grid, nt>>>(it, o)), threads * it, "G ops/s");
   TIME("smem LDS random", (k_smem<2><<<grid, nt>>>(it, o)), threads * it, "G ops/s");
