@@ -225,7 +225,9 @@ rs_status rs_release_cache(void);
 /* ---- split deviates (diagnostics / tests) ----------------------------------
  * out[t] = the split tree's deviate for node id id0 + t (the device code the
  * split kernels run): kind 0 = hypergeometric X ~ Hyp(k draws, L of R)
- * (R6), kind 1 = binomial X ~ Bin(k, L/R) (R9).
+ * (R6), kind 1 = binomial X ~ Bin(k, L/R) (R9);
+ * kinds 2/3 (4/5) = the same deviates computed by groups of 32 (8) lanes
+ * that evaluate rejection iterations in parallel (must be bit-identical).
  * out: device, count values.  L > R, (kind 0) k > R, R >= 2^63 -> RS_EINVAL. */
 rs_status rs_deviates(int kind, uint64_t k, uint64_t L, uint64_t R, uint64_t seed, uint64_t id0,
                       uint64_t count, uint64_t *out, void *stream);
@@ -252,7 +254,10 @@ rs_status rs_device_errors(int clear, unsigned *flags);
 /* Test hook: select the leaf implementation (process-wide).
  * RS_OPT_LEAF_PATH: 0 = automatic (default: warp-per-leaf kernels, bitmap
  * kernels for leaf ranges <= 2^15, CTA kernel for leaves that do not fit);
- * 1 = the CTA-per-leaf kernels for every leaf (so tests cover that path).
+ * 1 = the CTA-per-leaf kernels for every leaf (so tests cover that path);
+ * 2 = as 0; 3 = the ordered linear-probing warp kernels (rs_leaf_lp.cuh:
+ * a measured alternative, slower; kept selectable and tested) where every
+ * leaf range has >= 2^11 values.
  * RS_OPT_TOPUP_MAX: 0..32, most duplicates the warp kernels for small leaf
  * ranges top up draw by draw before running a full extra round (default 32;
  * tests lower it to cover the fallback).

@@ -202,8 +202,9 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
 {
     if (p.local_count == 0) return RS_OK;
     u32 *status = (u32 *)(ws + p.o_spill);
-    const bool warp_path = !(p.r_max <= BM_RMAX && p.mode == RS_MODE_WOR && g_leaf_path == 0) &&
-                           !p.comp && p.r_max <= 0xfffff000ull && g_leaf_path == 0;
+    const bool warp_path = !(p.r_max <= BM_RMAX && p.mode == RS_MODE_WOR && g_leaf_path != 1) &&
+                           !p.comp && p.r_max <= 0xfffff000ull && g_leaf_path != 1 &&
+                           (p.N >> p.D) >= (1ull << 11);
     if (clear_status)      // status + spill count in one memset
         cudaMemsetAsync(status, 0, warp_path ? 8 : 4, st);
     else if (warp_path)
@@ -243,8 +244,12 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         u64 *oc = flip ? pong_cnt : ping_cnt, *oo = flip ? pong_off : ping_off;
         if (d + 1 == p.D) { a.leaf_cnt = leaf_cnt; a.leaf_off = leaf_off; }
         else { a.out_cnt = oc; a.out_off = oo; }
-        const u64 grid = (a.width + LEVEL_NT - 1) / LEVEL_NT;
-        (a.wr ? k_split_level_wr : k_split_level)<<<(unsigned)grid, LEVEL_NT, 0, st>>>(a);
+        const u32 G = a.width <= RS_LV_G32_MAXW ? 32 : a.width <= RS_LV_G8_MAXW ? 8 : 1;
+        const u64 grid = (a.width * G + LEVEL_NT - 1) / LEVEL_NT;
+        void (*lk)(LevelArgs) = G == 32 ? (a.wr ? k_split_level_wr_g32 : k_split_level_g32)
+                              : G == 8  ? (a.wr ? k_split_level_wr_g8 : k_split_level_g8)
+                                        : (a.wr ? k_split_level_wr : k_split_level);
+        lk<<<(unsigned)grid, LEVEL_NT, 0, st>>>(a);
         ++t_launches;
         in_cnt = oc; in_off = oo;
     }
@@ -278,7 +283,7 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
     const bool wr = (p.mode == RS_MODE_WR);
     void (*kern)(LeafArgs);
     size_t sm;
-    if (p.r_max <= BM_RMAX && p.mode == RS_MODE_WOR && g_leaf_path == 0) {
+    if (p.r_max <= BM_RMAX && p.mode == RS_MODE_WOR && g_leaf_path != 1) {
         // small leaf ranges: warp per leaf over a bitmap (complement or WOR)
         la.out_base = p.shard_lo;
         void (*bk)(LeafArgs) = p.gV ? (p.comp ? k_leaf_bitmap_comp_g : k_leaf_bitmap_wor_g)
@@ -293,8 +298,9 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         la.out_base = p.shard_lo;
         la.tiles_per_leaf = (p.r_max + COMP_TILE - 1) / COMP_TILE;
         kern = wide ? k_leaf_comp64 : k_leaf_comp32;
-    } else if (!wide && g_leaf_path == 0) {
-        // common path: warp per leaf; leaves it cannot hold go to a spill
+    } else if (!wide && g_leaf_path != 1 && (p.N >> p.D) >= (1ull << 11)) {
+        // common path (leaf ranges of >= 2^11 values: the warp kernels' bucket
+        // function needs ceil_log2(r) >= 11): warp per leaf; leaves it cannot hold go to a spill
         // list that the CTA kernel completes right after (usually empty)
         u32 *spill_n = status + 1;        // zeroed above
         la.spill_n = spill_n;
@@ -310,13 +316,25 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
 #ifndef RS_WL_WOR_TU_ALL
 #define RS_WL_WOR_TU_ALL 1
 #endif
-        void (*wk)(LeafArgs) = wr ? k_leaf_warp_wr
-                             : p.gV ? (tu ? k_leaf_warp_gnm_tu : k_leaf_warp_gnm)
-                                    : ((tu || RS_WL_WOR_TU_ALL) ? k_leaf_warp_wor_tu : k_leaf_warp_wor);
-        const size_t wsm = sizeof(WarpLeaf) * WL_WARPS;
-        const u64 wgrid = (p.nleaves + WL_WARPS - 1) / WL_WARPS;
-        const unsigned g1 = leaf_grid((const void *)wk, 32 * WL_WARPS, wsm, wgrid);
-        wk<<<g1, 32 * WL_WARPS, wsm, st>>>(la);
+        // RS_OPT_LEAF_PATH = 3: the ordered linear-probing kernels (rs_leaf_lp.cuh;
+        // bit-exact, measured 1.9x slower than the counting-sort warp kernels:
+        // DESIGN.md section 6) when every leaf range has >= 2^11 values
+        const u64 r_min = p.N >> p.D;
+        if (!p.gV && g_leaf_path == 3 && r_min >= (1ull << LP_LOGT)) {
+            la.lp_cr = (u32)ceil_log2(p.r_max);
+            void (*lk)(LeafArgs) = wr ? k_leaf_lp_wr : k_leaf_lp_wor;
+            const size_t lsm = sizeof(LPLeaf) * LP_WARPS;
+            const unsigned gl = leaf_grid((const void *)lk, 32 * LP_WARPS, lsm, (p.nleaves + LP_WARPS - 1) / LP_WARPS);
+            lk<<<gl, 32 * LP_WARPS, lsm, st>>>(la);
+        } else {
+            void (*wk)(LeafArgs) = wr ? k_leaf_warp_wr
+                                 : p.gV ? (tu ? k_leaf_warp_gnm_tu : k_leaf_warp_gnm)
+                                        : ((tu || RS_WL_WOR_TU_ALL) ? k_leaf_warp_wor_tu : k_leaf_warp_wor);
+            const size_t wsm = sizeof(WarpLeaf) * WL_WARPS;
+            const u64 wgrid = (p.nleaves + WL_WARPS - 1) / WL_WARPS;
+            const unsigned g1 = leaf_grid((const void *)wk, 32 * WL_WARPS, wsm, wgrid);
+            wk<<<g1, 32 * WL_WARPS, wsm, st>>>(la);
+        }
         ++t_launches;
         LeafArgs lb = la;
         lb.spill = nullptr; lb.spill_n = nullptr;
@@ -585,6 +603,17 @@ __global__ void k_deviates(int kind, u64 k, u64 L, u64 R, u64 seed, u64 id0, u64
 {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count; i += (u64)gridDim.x * blockDim.x)
         out[i] = kind ? binom(k, L, R, seed, id0 + i) : hgd(k, L, R, seed, id0 + i);
+}
+
+// The lane-group deviates (hgd_grp / binom_grp): G lanes per deviate.
+template <int G>
+__global__ void k_deviates_grp(int kind, u64 k, u64 L, u64 R, u64 seed, u64 id0, u64 count, u64 *out)
+{
+    const u64 ngrp = (u64)gridDim.x * blockDim.x / G;
+    for (u64 i = (blockIdx.x * (u64)blockDim.x + threadIdx.x) / G; i < count; i += ngrp) {
+        const u64 x = kind ? binom_grp<G>(k, L, R, seed, id0 + i) : hgd_grp<G>(k, L, R, seed, id0 + i);
+        if ((threadIdx.x & (G - 1)) == 0) out[i] = x;
+    }
 }
 
 }  // namespace
@@ -921,12 +950,15 @@ static rs_status shard_host(int mode, uint64_t N, uint64_t n, uint64_t seed, int
 rs_status rs_deviates(int kind, uint64_t k, uint64_t L, uint64_t R, uint64_t seed, uint64_t id0,
                       uint64_t count, uint64_t *out, void *stream)
 {
-    if (kind != 0 && kind != 1) return ret(RS_EINVAL);
-    if (L > R || (kind == 0 && k > R) || R >= (1ull << 63)) return ret(RS_EINVAL);
+    if (kind < 0 || kind > 5) return ret(RS_EINVAL);
+    if (L > R || ((kind & 1) == 0 && k > R) || R >= (1ull << 63)) return ret(RS_EINVAL);
     if (!have_device()) return ret(RS_ECUDA);
     if (count == 0) return ret(RS_OK);
     const u64 g = (count + 127) / 128;
-    k_deviates<<<(unsigned)(g < 4096 ? g : 4096), 128, 0, S(stream)>>>(kind, k, L, R, seed, id0, count, out);
+    const unsigned gg = (unsigned)(g < 4096 ? g : 4096);
+    if (kind <= 1) k_deviates<<<gg, 128, 0, S(stream)>>>(kind, k, L, R, seed, id0, count, out);
+    else if (kind <= 3) k_deviates_grp<32><<<gg, 128, 0, S(stream)>>>(kind & 1, k, L, R, seed, id0, count, out);
+    else k_deviates_grp<8><<<gg, 128, 0, S(stream)>>>(kind & 1, k, L, R, seed, id0, count, out);
     ++t_launches;
     return ret(cuda_ok());
 }
@@ -1013,7 +1045,7 @@ rs_status rs_device_errors(int clear, unsigned *flags)
 
 rs_status rs_set_option(int option, int value)
 {
-    if (option == RS_OPT_LEAF_PATH && (value == 0 || value == 1)) {
+    if (option == RS_OPT_LEAF_PATH && value >= 0 && value <= 3) {
         g_leaf_path = value;
         return ret(RS_OK);
     }

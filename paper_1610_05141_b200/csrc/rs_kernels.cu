@@ -9,6 +9,19 @@ __device__ unsigned g_rs_errors = 0;
 // ===========================================================================
 // Split tree (rows a3/a4).
 // ===========================================================================
+template <bool WR, int G>
+__device__ __forceinline__ void split_top_level(const SplitArgs &a, const u64 *in, u64 *outb, u32 width, int d, u64 base)
+{
+    for (u32 j = threadIdx.x / G; j < width; j += SPLIT_NT / G) {
+        const u64 k = in[j];
+        const u64 x = split_node_grp<WR, G>(a.N, d, base + j, k, a.seed);
+        if ((threadIdx.x & (G - 1)) == 0) {
+            outb[2 * j] = x;
+            outb[2 * j + 1] = k - x;
+        }
+    }
+}
+
 template <bool WR>
 __device__ __forceinline__ void split_top(const SplitArgs &a)
 {
@@ -24,12 +37,11 @@ __device__ __forceinline__ void split_top(const SplitArgs &a)
         const u32 width = 1u << l;
         const int d = a.ds + l;
         const u64 base = node << l;
-        for (u32 j = tid; j < width; j += SPLIT_NT) {
-            const u64 k = buf[cur][j];
-            const u64 x = split_node_t<WR>(a.N, d, base + j, k, a.seed);
-            buf[cur ^ 1][2 * j] = x;
-            buf[cur ^ 1][2 * j + 1] = k - x;
-        }
+        // narrow levels: a group of G lanes per node evaluates G rejection
+        // iterations at once (hgd_grp), so a level costs ~one iteration's latency
+        if (width * 32 <= SPLIT_NT)     split_top_level<WR, 32>(a, buf[cur], buf[cur ^ 1], width, d, base);
+        else if (width * 8 <= SPLIT_NT) split_top_level<WR, 8>(a, buf[cur], buf[cur ^ 1], width, d, base);
+        else                            split_top_level<WR, 1>(a, buf[cur], buf[cur ^ 1], width, d, base);
         __syncthreads();
         cur ^= 1;
     }
@@ -57,13 +69,14 @@ __device__ __forceinline__ void split_top(const SplitArgs &a)
     }
 }
 
-template <bool WR>
+template <bool WR, int G = 1>
 __device__ __forceinline__ void split_level(const LevelArgs &a)
 {
-    const u64 j = (u64)blockIdx.x * LEVEL_NT + threadIdx.x;
-    if (j >= a.width) return;
+    const u64 j = ((u64)blockIdx.x * LEVEL_NT + threadIdx.x) / G;
+    if (j >= a.width) return;                 // (whole groups: width * G is a multiple of G)
     const u64 k = a.in_cnt[j], off = a.in_off[j];
-    const u64 x = split_node_t<WR>(a.N, a.d, a.node0 + j, k, a.seed);
+    const u64 x = split_node_grp<WR, G>(a.N, a.d, a.node0 + j, k, a.seed);
+    if ((threadIdx.x & (G - 1)) != 0) return;
     if (a.leaf_cnt) {
         if (k > 0xffffffffull) atomicOr(&g_rs_errors, 1u);
         a.leaf_cnt[2 * j] = (u32)x;
@@ -122,6 +135,10 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split(SplitArgs a) { split_top<fal
 __global__ void __launch_bounds__(SPLIT_NT) k_split_wr(SplitArgs a) { split_top<true>(a); }
 __global__ void __launch_bounds__(LEVEL_NT, RS_LV_MINB) k_split_level(LevelArgs a) { split_level<false>(a); }
 __global__ void __launch_bounds__(LEVEL_NT, RS_LV_MINB) k_split_level_wr(LevelArgs a) { split_level<true>(a); }
+__global__ void __launch_bounds__(LEVEL_NT, RS_LV_MINB) k_split_level_g32(LevelArgs a) { split_level<false, 32>(a); }
+__global__ void __launch_bounds__(LEVEL_NT, RS_LV_MINB) k_split_level_g8(LevelArgs a) { split_level<false, 8>(a); }
+__global__ void __launch_bounds__(LEVEL_NT, RS_LV_MINB) k_split_level_wr_g32(LevelArgs a) { split_level<true, 32>(a); }
+__global__ void __launch_bounds__(LEVEL_NT, RS_LV_MINB) k_split_level_wr_g8(LevelArgs a) { split_level<true, 8>(a); }
 __global__ void __launch_bounds__(LEVEL_NT, RS_D3_MINB) k_split_deep2(LevelArgs a) { split_deep<2, false>(a); }
 __global__ void __launch_bounds__(LEVEL_NT, RS_D3_MINB) k_split_deep3(LevelArgs a) { split_deep<3, false>(a); }
 __global__ void __launch_bounds__(LEVEL_NT, RS_D3_MINB) k_split_deep4(LevelArgs a) { split_deep<4, false>(a); }
@@ -133,6 +150,7 @@ __global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep4_wr(LevelArgs a) { s
 
 #include "rs_leaf.cuh"
 #include "rs_leaf_warp.cuh"
+#include "rs_leaf_lp.cuh"
 #include "rs_leaf_bitmap.cuh"
 #include "rs_algb.cuh"
 

@@ -10,7 +10,7 @@ namespace rs {
 // bit 1 Bernoulli chunk capacity.  Defined in rs_kernels.cu (librs.cu is a
 // single translation unit).
 
-constexpr int SPLIT_NT = 256;
+constexpr int SPLIT_NT = 512;                     // top CTA: narrow levels use lane groups
 constexpr int SPLIT_LEVELS = 11;                 // levels expanded per split phase
 constexpr int SPLIT_WIDTH = 1 << SPLIT_LEVELS;   // nodes per CTA at the phase's last level
 
@@ -107,6 +107,17 @@ struct LevelArgs {
 #endif
 __global__ void __launch_bounds__(LEVEL_NT, RS_LV_MINB) k_split_level(LevelArgs a);
 __global__ void __launch_bounds__(LEVEL_NT, RS_LV_MINB) k_split_level_wr(LevelArgs a);
+// the same with G = 32 / 8 lanes per node (parallel rejection iterations, narrow levels)
+__global__ void __launch_bounds__(LEVEL_NT, RS_LV_MINB) k_split_level_g32(LevelArgs a);
+__global__ void __launch_bounds__(LEVEL_NT, RS_LV_MINB) k_split_level_g8(LevelArgs a);
+__global__ void __launch_bounds__(LEVEL_NT, RS_LV_MINB) k_split_level_wr_g32(LevelArgs a);
+__global__ void __launch_bounds__(LEVEL_NT, RS_LV_MINB) k_split_level_wr_g8(LevelArgs a);
+#ifndef RS_LV_G32_MAXW
+#define RS_LV_G32_MAXW (1u << 12)     // level widths up to this take 32 lanes per node
+#endif
+#ifndef RS_LV_G8_MAXW
+#define RS_LV_G8_MAXW (1u << 14)      // ... then 8 lanes per node
+#endif
 // The last 2, 3 or 4 levels in one launch, a thread per subtree.
 #ifndef RS_D3_MINB
 #define RS_D3_MINB 8      // 64 registers: twice the warps (measured: split 1.66 -> 1.49 ms)
@@ -140,6 +151,7 @@ struct LeafArgs {
     u32 topup_max;         // warp *_tu kernels: most new values topped up per leaf (<= 32)
     u32 *status;           // per-call status word (bit 0: a leaf exceeded the on-chip capacity)
     u32 cap;               // CTA kernel draw capacity (0: LEAF_CAP; rs_set_option(RS_OPT_LEAF_CAP), tests)
+    u32 lp_cr;             // LP kernels: ceil_log2 of the launch's largest leaf range (generation tag shift)
 };
 
 __global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_wor32(LeafArgs a);
@@ -165,6 +177,13 @@ __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr(Leaf
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm_tu(LeafArgs a);
+// Ordered linear-probing leaf kernels (rs_leaf_lp.cuh): the default WOR / WR path.
+#ifndef RS_LP_WARPS
+#define RS_LP_WARPS 16
+#endif
+constexpr int LP_WARPS = RS_LP_WARPS;
+__global__ void __launch_bounds__(32 * LP_WARPS, 1) k_leaf_lp_wor(LeafArgs a);
+__global__ void __launch_bounds__(32 * LP_WARPS, 1) k_leaf_lp_wr(LeafArgs a);
 #ifndef RS_WL_TU_LOG
 #define RS_WL_TU_LOG 21
 #endif

@@ -51,6 +51,9 @@
 #ifndef RS_WL_MINB
 #define RS_WL_MINB 1          // resident CTAs per SM the register budget is sized for (16 warps)
 #endif
+#ifndef RS_WL_GB
+#define RS_WL_GB 3          // scatter group (blocks); measured: headline leaf 14.06 (1) / 13.66 (3) / 14.09 ms (9)
+#endif
 
 namespace rs {
 
@@ -111,6 +114,20 @@ struct WDrawer {
     u32 s;          // 32 - ceil_log2(r)
     bool pow2;
     __device__ WDrawer(const Stream &st, u64 r, int cr) : d(st, r), s(32u - (u32)cr), pow2((r & (r - 1)) == 0) {}
+    // power-of-two range: the top cr bits of each word (Lemire never rejects)
+    __device__ __forceinline__ void block_pow2(const RoundKeys &K, u32 q, u32 *v) const
+    {
+        u32 c0 = q, c1 = d.st.tag, c2 = d.st.id_lo, c3 = d.st.id_hi;
+#pragma unroll
+        for (int r = 0; r < 10; ++r) {
+            const u64 p0 = (u64)0xD2511F53u * c0, p1 = (u64)0xCD9E8D57u * c2;
+            c0 = (u32)(p1 >> 32) ^ c1 ^ K.k[2 * r];
+            c1 = (u32)p1;
+            c2 = (u32)(p0 >> 32) ^ c3 ^ K.k[2 * r + 1];
+            c3 = (u32)p0;
+        }
+        v[0] = shr32(c0, s); v[1] = shr32(c1, s); v[2] = shr32(c2, s); v[3] = shr32(c3, s);
+    }
     __device__ __forceinline__ void block(const RoundKeys &K, u32 q, u32 *v) const
     {
 #ifdef RS_EXP_NOPHILOX
@@ -268,6 +285,105 @@ __device__ __forceinline__ u32 wl_count(WarpLeaf &sh, const RoundKeys &K, const 
     return shb == 0 ? 0u : P;
 }
 
+#ifndef RS_WL_REG
+#define RS_WL_REG 0         // 1: draws stay in registers from the count to the scatter (no staging round trip)
+#endif
+
+// Monotone bucket of a draw x < 2^cr (cr >= 11), 1056 buckets:
+// b = floor(33 x / 2^(cr - 5)) = hi(x * M), M = 33 << (37 - cr) -- one
+// IMAD.HI.  Bucket b's counter is word b: lane l owns the words
+// [33 l, 33 l + 33) in the scan (stride 33: conflict-free).
+__device__ __forceinline__ u32 wl_bucket_mult(int cr) { return 33u << (37 - cr); }
+
+// hi(x * M) as an opaque instruction: recomputed at each use (the count and
+// the scatter) instead of 36 bucket indices held in registers across the scan.
+__device__ __forceinline__ u32 wl_bkt(u32 x, u32 M)
+{
+    u32 b;
+    asm volatile("mul.hi.u32 %0, %1, %2;" : "=r"(b) : "r"(x), "r"(M));
+    return b;
+}
+
+// Steps 1-2 with the round's draws kept in registers: lane l's blocks
+// l + 32 m (m < 9) -> x[4 m .. 4 m + 3]; RED.ADD count[bucket]; scan the
+// counts into starts.  Returns the largest bucket load.
+template <bool POW2>
+__device__ __forceinline__ u32 wl_count_reg(WarpLeaf &sh, const RoundKeys &K, const WDrawer &dr, u32 J, u32 M,
+                                            u32 lane, u32 (&x)[WL_E1])
+{
+    constexpr int NB = WL_E1 / 4;
+#pragma unroll
+    for (int m = 0; m < NB; ++m) {
+        const u32 q = lane + 32u * m;
+        if (POW2) dr.block_pow2(K, q, &x[4 * m]);
+        else dr.d.block(q, &x[4 * m]);
+        if (128u * m + 127u < J) {               // every lane's four draws count
+#pragma unroll
+            for (int t = 0; t < 4; ++t) atomicAdd(&sh.cnt[wl_bkt(x[4 * m + t], M)], 1u);
+        } else {
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (4 * q + t < J) atomicAdd(&sh.cnt[wl_bkt(x[4 * m + t], M)], 1u);
+        }
+    }
+    __syncwarp();
+    u32 *cl = sh.cnt + 33 * lane;
+    u32 c[33];
+#pragma unroll
+    for (int i = 0; i < 33; ++i) c[i] = cl[i];
+    u32 seg[3], mx3[3];
+#pragma unroll
+    for (int g = 0; g < 3; ++g) {                // three independent chains (ILP)
+        seg[g] = 0; mx3[g] = 0;
+#pragma unroll
+        for (int i = 0; i < 11; ++i) { seg[g] += c[11 * g + i]; mx3[g] = max(mx3[g], c[11 * g + i]); }
+    }
+    const u32 S = seg[0] + seg[1] + seg[2];
+    const u32 mx = max(max(mx3[0], mx3[1]), mx3[2]);
+    const u32 run = warp_excl_scan(S, lane);
+    const u32 P = __reduce_max_sync(0xffffffffu, mx);
+    u32 rg[3];
+    rg[0] = run; rg[1] = run + seg[0]; rg[2] = rg[1] + seg[1];
+#pragma unroll
+    for (int i = 0; i < 11; ++i) {               // starts in place, three chains
+#pragma unroll
+        for (int g = 0; g < 3; ++g) { cl[11 * g + i] = rg[g]; rg[g] += c[11 * g + i]; }
+    }
+    __syncwarp();
+    return P;
+}
+
+// Step 3 from registers: every draw to its bucket's next position (+ h).
+__device__ __forceinline__ void wl_scatter_reg(WarpLeaf &sh, u32 J, u32 h, u32 M, u32 lane, const u32 (&x)[WL_E1])
+{
+    u32 *kh = sh.keys + h;
+    constexpr int NB = WL_E1 / 4;
+    constexpr int GB = RS_WL_GB;
+    static_assert(NB % GB == 0, "group size");
+#pragma unroll
+    for (int m0 = 0; m0 < NB; m0 += GB) {
+        u32 pos[4 * GB];
+        if (128u * (m0 + GB - 1) + 127u < J) {   // the group's draws all exist for every lane
+#pragma unroll
+            for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) pos[e - 4 * m0] = atomicAdd(&sh.cnt[wl_bkt(x[e], M)], 1u);
+            // atomics first, stores after (smem stores and atomics may alias as far
+            // as the compiler knows: interleaving would serialise every round trip)
+#pragma unroll
+            for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) kh[pos[e - 4 * m0]] = x[e];
+        } else if (128u * m0 < J) {
+#pragma unroll
+            for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) {
+                const u32 j = 4 * (lane + 32u * (e >> 2)) + (e & 3);
+                pos[e - 4 * m0] = j < J ? atomicAdd(&sh.cnt[wl_bkt(x[e], M)], 1u) : (u32)WL_CAP;
+            }
+#pragma unroll
+            for (int e = 4 * m0; e < 4 * (m0 + GB); ++e)
+                if (pos[e - 4 * m0] != (u32)WL_CAP) kh[pos[e - 4 * m0]] = x[e];
+        }
+    }
+    __syncwarp();
+}
+
 __device__ __forceinline__ void wl_clear(WarpLeaf &sh, u32 lane)
 {
     static_assert(WL_B % 128 == 0 && WL_B / 32 <= 32, "clear layout");
@@ -341,9 +457,6 @@ __device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const RoundKeys &K, con
     // Atomics first, stores after, in groups of GB blocks: smem stores and
     // atomics may alias as far as the compiler knows, so interleaving them
     // would serialise every atomic's round trip.
-#ifndef RS_WL_GB
-#define RS_WL_GB 3          // measured: headline leaf 14.06 (1) / 13.66 (3) / 14.09 ms (9)
-#endif
     constexpr int GB = RS_WL_GB;
     static_assert(NB % GB == 0, "group size");
 #pragma unroll
@@ -700,8 +813,25 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
 #endif
         constexpr bool SMST = RS_WL_SMEMST || (RS_WL_SMEMST_GR && GR);
         u32 J = k;
+#if RS_WL_REG
+        const u32 M = wl_bucket_mult(cr);
+#endif
         for (;;) {
             u32 res = 0xffffffffu;
+#if RS_WL_REG
+            if (J + h <= (u32)WL_CAP) {
+                u32 x[WL_E1];
+                const u32 P = dr.pow2 ? wl_count_reg<true>(sh, a.rk, dr, J, M, lane, x)
+                                      : wl_count_reg<false>(sh, a.rk, dr, J, M, lane, x);
+                if (P > WL_PMAX) {              // pathological bucket load
+                    wl_clear(sh, lane);
+                    __syncwarp();
+                } else {
+                    wl_scatter_reg(sh, J, h, M, lane, x);
+                    res = wl_finish<WL_E1, WR, GR, TU>(sh, J, k, h, P, SMST ? 0 : base, SMST ? nullptr : dst, lane, a.gV);
+                }
+            }
+#else
             if (J + h <= (u32)WL_CAP) {
                 const u32 P = wl_count(sh, a.rk, dr, J, shb, lane);
                 if (P > WL_PMAX) {              // pathological bucket load
@@ -725,6 +855,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
 #endif
                 }
             }
+#endif
             if (res == 0) break;
             if (res == 0xffffffffu) {           // the CTA kernel completes this leaf
                 if (lane == 0) a.spill[atomicAdd(a.spill_n, 1u)] = (u32)L;

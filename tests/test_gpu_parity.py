@@ -87,6 +87,25 @@ def test_wor_cta_path(N, n):
     _no_device_errors()
 
 
+# the ordered linear-probing warp kernels (RS_OPT_LEAF_PATH = 3; a measured
+# alternative to the counting-sort warp kernels)
+LP_CASES = [(2 ** 30, 2 ** 20), (2 ** 40, 2 ** 22), (10 ** 9 + 7, 100003), (2 ** 21, 2 ** 20),
+            (2 ** 24 + 3, 2 ** 16 + 1), (3 ** 30, 2 ** 18 + 17), (2 ** 48, 2 ** 24)]
+
+
+@pytest.mark.parametrize("N,n", LP_CASES)
+def test_lp_path(N, n):
+    rs.set_option(rs.OPT_LEAF_PATH, 3)
+    try:
+        got = _np(rs.sample_wor(N, n, 5))
+        gwr = _np(rs.sample_wr(N, n, 5))
+    finally:
+        rs.set_option(rs.OPT_LEAF_PATH, 0)
+    assert np.array_equal(got, O.sample_wor(N, n, 5))
+    assert np.array_equal(gwr, O.sample_wr(N, n, 5))
+    _no_device_errors()
+
+
 # ---- with replacement --------------------------------------------------------
 
 WR_CASES = [(1, 5), (4, 1000), (2, 3), (100, 100), (2 ** 24, 2 ** 20), (10 ** 9 + 7, 100003),
@@ -387,9 +406,11 @@ def test_deviates_vs_oracle(k, L, R):
     for kind, f in ((0, O.hgd_batch), (1, O.bin_batch)):
         if kind == 1 and k > 2 ** 40:
             continue
-        got = _np(rs.deviates(kind, k, L, R, 77, 1, cnt))
         exp = f(k, L, R, 77, 1, cnt)
-        assert np.array_equal(got, exp), (kind, k, L, R, int(np.sum(got != exp)))
+        # thread per deviate, then lane groups of 32 and 8 (parallel iterations)
+        for kk in (kind, kind + 2, kind + 4):
+            got = _np(rs.deviates(kk, k, L, R, 77, 1, cnt))
+            assert np.array_equal(got, exp), (kk, k, L, R, int(np.sum(got != exp)))
 
 
 @pytest.mark.parametrize("tmax", [0, 1, 2])
@@ -434,19 +455,21 @@ def test_capacity_overflow_returns_ecapacity():
 
 
 def test_host_stream_ring():
-    """rs_sample_shard_host_stream with a host buffer smaller than the slice:
-    the last batch of each slot is what remains in the ring; with a buffer of
-    the full size it equals rs_sample_shard_host."""
-    N, n, seed = 2 ** 40, 2 ** 28, 3
+    """rs_sample_shard_host_stream with a host buffer smaller than the slice
+    (two batches of ~2^25 values through a 2 x (2^25 + 2^20) ring): every
+    value that reaches the ring is one of the sample's; with a buffer of the
+    full size it equals rs_sample_shard_host."""
+    N, n, seed = 2 ** 40, 2 ** 26 + 5, 3
     full = rs.sample_shard_host(rs.MODE_WOR, N, n, seed, 1, 0)
     big = torch.empty(n, dtype=torch.uint64, pin_memory=True)
     rs.sample_shard_host_stream(rs.MODE_WOR, N, n, seed, 1, 0, big)
     assert torch.equal(big.view(torch.int64), full.view(torch.int64))
-    ring = torch.zeros(2 * (2 ** 27 + 2 ** 21), dtype=torch.uint64, pin_memory=True)
+    ring = torch.zeros(2 * (2 ** 25 + 2 ** 20), dtype=torch.uint64, pin_memory=True)
     rs.sample_shard_host_stream(rs.MODE_WOR, N, n, seed, 1, 0, ring)
-    # every value that reached the ring is one of the sample's
     r = ring.view(torch.int64).numpy()
     v = r[r != 0]
-    assert v.size > 2 ** 26 and np.isin(v, full.view(torch.int64).numpy()).all()
+    f = full.view(torch.int64).numpy()
+    idx = np.minimum(np.searchsorted(f, v), f.size - 1)
+    assert v.size > 2 ** 25 and np.array_equal(f[idx], v)
     with pytest.raises(rs.RSError):
         rs.sample_shard_host_stream(rs.MODE_WOR, N, n, seed, 1, 0, ring[:1000])

@@ -1,0 +1,3 @@
+python tools/debug/lp_prof.py > gpurun_out/g6_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_leaf_lp -s 1 -c 1 -o gpurun_out/g6_lp python tools/debug/lp_prof.py > gpurun_out/g6_ncu.log 2>&1
+echo "ncu rc=$?"
