@@ -407,11 +407,12 @@ def run_native(args):
                 kname += "_tu"
     kms_per = kms / max(kl, 1)
     achieved = bytes_per_launch / (kms_per / 1e3) / 1e9 if kms_per > 0 else None
-    traffic = None
+    traffic, winst = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f).get(wl["name"])
             traffic = float(t["bytes_per_launch"]) if t else None
+            winst = float(t["warp_inst_per_launch"]) if t and t.get("warp_inst_per_launch") else None
     except Exception:
         pass
     # write-only ceiling on the same buffer: torch's vectorised fill of the
@@ -439,6 +440,19 @@ def run_native(args):
                 "step_share": kms / max(args.steps, 1) / ms if ms > 0 else None,
                 "split_ms": kt["split"][0] / max(args.steps, 1),
                 "classes_ms": {k: v[0] / max(args.steps, 1) for k, v in kt.items()}}
+    # second ceiling: instruction issue.  Warp instructions per
+    # launch from the committed ncu capture (profiles/traffic.json) over the
+    # live kernel time, against 4 warp-instructions / SM / cycle (one per
+    # SMSP; tools/ubench measures 3.95 for an ALU+FMA mix) at the sampled SM clock
+    csum0 = clocks.summary()
+    f_sm = (csum0.get("sm_mhz") or 1965.0) * 1e6
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    if winst and kms_per > 0:
+        ipc = winst / (kms_per / 1e3) / (nsm * f_sm)
+        roofline["issue"] = {"warp_inst_per_launch": winst,
+                             "warp_inst_per_sample": winst / max(float(n_local_done), 1.0),
+                             "achieved_ipc_per_sm": ipc, "peak_ipc_per_sm": 4.0, "frac": ipc / 4.0,
+                             "sm_mhz": f_sm / 1e6, "source": "profiles/traffic.json (ncu smsp__inst_executed.sum)"}
 
     # ---- end to end through the C ABI with a host buffer (fewer steps)
     e2e = None

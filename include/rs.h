@@ -226,8 +226,10 @@ rs_status rs_release_cache(void);
  * out[t] = the split tree's deviate for node id id0 + t (the device code the
  * split kernels run): kind 0 = hypergeometric X ~ Hyp(k draws, L of R)
  * (R6), kind 1 = binomial X ~ Bin(k, L/R) (R9);
- * kinds 2/3 (4/5) = the same deviates computed by groups of 32 (8) lanes
- * that evaluate rejection iterations in parallel (must be bit-identical).
+ * kinds 2/3 (4/5) = the same deviates computed by groups of 32 (8) lanes:
+ * hypergeometric with 32 lanes splits the work by density term (hgd_tp),
+ * otherwise the lanes evaluate rejection iterations in parallel -- all must
+ * be bit-identical to kinds 0/1.
  * out: device, count values.  L > R, (kind 0) k > R, R >= 2^63 -> RS_EINVAL. */
 rs_status rs_deviates(int kind, uint64_t k, uint64_t L, uint64_t R, uint64_t seed, uint64_t id0,
                       uint64_t count, uint64_t *out, void *stream);
@@ -261,12 +263,14 @@ rs_status rs_device_errors(int clear, unsigned *flags);
  * RS_OPT_TOPUP_MAX: 0..32, most duplicates the warp kernels for small leaf
  * ranges top up draw by draw before running a full extra round (default 32;
  * tests lower it to cover the fallback).
+ * RS_OPT_SPLIT_COOP: 1 (default) = the narrow top of the split tree in one
+ * cooperative launch; 0 = a single top CTA then one launch per level.
  * RS_OPT_LEAF_CAP: 0 (default) or 1..2048, the CTA leaf kernel's draw
  * capacity; small values force capacity overflows so that tests can check
  * that they are reported (RS_ECAPACITY from the checked calls).
  * Results are identical for every setting of the first two (the third
  * changes which leaves fail).  Unknown option or value -> RS_EINVAL. */
-enum { RS_OPT_LEAF_PATH = 1, RS_OPT_TOPUP_MAX = 2, RS_OPT_LEAF_CAP = 3 };
+enum { RS_OPT_LEAF_PATH = 1, RS_OPT_TOPUP_MAX = 2, RS_OPT_LEAF_CAP = 3, RS_OPT_SPLIT_COOP = 4 };
 rs_status rs_set_option(int option, int value);
 
 /* Number of kernel launches issued by this thread since the last reset. */

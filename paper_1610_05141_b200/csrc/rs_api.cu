@@ -20,6 +20,10 @@ thread_local rs_status t_last = RS_OK;
 int g_leaf_path = 0;                    // rs_set_option(RS_OPT_LEAF_PATH)
 int g_topup_max = 32;                   // rs_set_option(RS_OPT_TOPUP_MAX)
 int g_leaf_cap = 0;                     // rs_set_option(RS_OPT_LEAF_CAP) (tests: force overflows)
+int g_split_coop = 1;                   // rs_set_option(RS_OPT_SPLIT_COOP): cooperative top of the split tree
+#ifndef RS_COOP_LEVELS
+#define RS_COOP_LEVELS 15               // input widths 1 .. 2^14
+#endif
 thread_local uint64_t t_launches = 0;
 
 rs_status ret(rs_status s) { t_last = s; return s; }
@@ -153,7 +157,7 @@ rs_status plan_node(int mode, u64 N, u64 n, u64 seed, int s, u64 idx, TreePlan &
     p.o_pong_off = o; o = align256(o + wmax * 8);
     p.o_leaf_cnt = o; o = align256(o + p.nleaves * 4);
     p.o_leaf_off = o; o = align256(o + p.nleaves * 8);
-    p.o_spill = o; o = align256(o + (p.nleaves + 2) * 4);   // status word, spill count + list
+    p.o_spill = o; o = align256(o + (p.nleaves + 4) * 4);   // status word, spill count, barrier, pad, spill list
     p.bytes = o;
     return RS_OK;
 }
@@ -202,19 +206,50 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
 {
     if (p.local_count == 0) return RS_OK;
     u32 *status = (u32 *)(ws + p.o_spill);
-    const bool warp_path = !(p.r_max <= BM_RMAX && p.mode == RS_MODE_WOR && g_leaf_path != 1) &&
-                           !p.comp && p.r_max <= 0xfffff000ull && g_leaf_path != 1 &&
-                           (p.N >> p.D) >= (1ull << 11);
-    if (clear_status)      // status + spill count in one memset
-        cudaMemsetAsync(status, 0, warp_path ? 8 : 4, st);
-    else if (warp_path)
-        cudaMemsetAsync(status + 1, 0, 4, st);
+    const bool warp_path = (!(p.r_max <= BM_RMAX && p.mode == RS_MODE_WOR && g_leaf_path != 1) &&
+                            !p.comp && p.r_max <= 0xfffff000ull && g_leaf_path != 1 &&
+                            (p.N >> p.D) >= (1ull << 11)) ||
+                           (!p.comp && p.r_max > 0xfffff000ull && g_leaf_path != 1 && !p.gV);   // wide warp path
+    (void)warp_path;
+    if (clear_status)      // status, spill count and the split's grid barrier in one memset
+        cudaMemsetAsync(status, 0, 16, st);
+    else
+        cudaMemsetAsync(status + 1, 0, 12, st);
     u64 *ping_cnt = (u64 *)(ws + p.o_ping_cnt), *ping_off = (u64 *)(ws + p.o_ping_off);
     u64 *pong_cnt = (u64 *)(ws + p.o_pong_cnt), *pong_off = (u64 *)(ws + p.o_pong_off);
     u32 *leaf_cnt = (u32 *)(ws + p.o_leaf_cnt);
     u64 *leaf_off = (u64 *)(ws + p.o_leaf_off);
     Span sp_split(0, st);
-    {   // top levels s .. s+top in one CTA
+    const u64 *in_cnt = ping_cnt, *in_off = ping_off;
+    int top = p.top;
+#ifndef RS_COOP_MIN_LEVELS
+#define RS_COOP_MIN_LEVELS 6            // shallower trees: the single top CTA (no grid barrier, smaller launch)
+#endif
+    if (g_split_coop && p.D - p.s >= RS_COOP_MIN_LEVELS) {   // the narrow top (input widths <= 2^14) in one cooperative launch
+        CoopArgs a;
+        memset(&a, 0, sizeof a);
+        a.N = p.N; a.seed = p.seed;
+        a.ds = p.s; a.D = p.D; a.node0 = p.idx; a.root_cnt = p.root_cnt;
+        a.nlev = (p.D - p.s) < RS_COOP_LEVELS ? (p.D - p.s) : RS_COOP_LEVELS;
+        a.buf_cnt[0] = ping_cnt; a.buf_off[0] = ping_off; a.buf_cnt[1] = pong_cnt; a.buf_off[1] = pong_off;
+        a.leaf_cnt = leaf_cnt; a.leaf_off = leaf_off;
+        a.bar = status + 2;                            // zeroed above
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            if (sms <= 0) sms = 148;
+        }
+        void *args[] = {&a};
+        const void *kf = (p.mode == RS_MODE_WR) ? (const void *)k_split_coop_wr : (const void *)k_split_coop;
+        if (cudaLaunchCooperativeKernel(kf, dim3(sms), dim3(COOP_NT), args, 0, st) != cudaSuccess) return RS_ECUDA;
+        ++t_launches;
+        top = a.nlev;
+        const int lastbuf = (a.nlev - 1) & 1;          // where level ds + nlev's counts are
+        in_cnt = lastbuf ? pong_cnt : ping_cnt;
+        in_off = lastbuf ? pong_off : ping_off;
+    } else {   // top levels s .. s+top in one CTA
         SplitArgs a;
         memset(&a, 0, sizeof a);
         a.N = p.N; a.seed = p.seed; a.wr = (p.mode == RS_MODE_WR);
@@ -225,22 +260,28 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         (a.wr ? k_split_wr : k_split)<<<1, SPLIT_NT, 0, st>>>(a);
         ++t_launches;
     }
-    const u64 *in_cnt = ping_cnt, *in_off = ping_off;
     // the last NL levels (when there are level kernels at all) in one launch,
     // a thread per depth-(D-NL) subtree
 #ifndef RS_SPLIT_DEEP
 #define RS_SPLIT_DEEP 3
 #endif
-    const int below = p.D - p.s - p.top;               // levels after the top CTA
-    const int NL = below >= RS_SPLIT_DEEP + 1 ? RS_SPLIT_DEEP : 0;
-    for (int d = p.s + p.top; d < p.D - NL; ++d) {    // one launch per level
+    const int below = p.D - p.s - top;                 // levels after the top
+    // (only where the deep levels are wide: a narrow subtree per thread is a
+    // chain of 2^NL - 1 sequential deviates, slower than NL lane-group levels)
+#ifndef RS_SPLIT_DEEP_MINW
+#define RS_SPLIT_DEEP_MINW (1ull << 15)
+#endif
+    const int NL = (below >= RS_SPLIT_DEEP + 1 && (1ull << (p.D - p.s - RS_SPLIT_DEEP)) >= RS_SPLIT_DEEP_MINW)
+                       ? RS_SPLIT_DEEP : 0;
+    const int flip0 = (in_cnt == pong_cnt) ? 1 : 0;   // the next output goes to the other buffer
+    for (int d = p.s + top; d < p.D - NL; ++d) {      // one launch per level
         LevelArgs a;
         memset(&a, 0, sizeof a);
         a.N = p.N; a.seed = p.seed; a.wr = (p.mode == RS_MODE_WR); a.d = d;
         a.width = 1ull << (d - p.s);
         a.node0 = p.idx << (d - p.s);
         a.in_cnt = in_cnt; a.in_off = in_off;
-        const bool flip = ((d - p.s - p.top) & 1) == 0;
+        const bool flip = (((d - p.s - top) & 1) == 0) != (flip0 == 1);
         u64 *oc = flip ? pong_cnt : ping_cnt, *oo = flip ? pong_off : ping_off;
         if (d + 1 == p.D) { a.leaf_cnt = leaf_cnt; a.leaf_off = leaf_off; }
         else { a.out_cnt = oc; a.out_off = oo; }
@@ -304,7 +345,7 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         // list that the CTA kernel completes right after (usually empty)
         u32 *spill_n = status + 1;        // zeroed above
         la.spill_n = spill_n;
-        la.spill = spill_n + 1;
+        la.spill = status + 4;
         // leaves with many duplicates (r <= 2^21: >= 22 % of leaves) top the
         // distinct set up draw by draw instead of re-running a full round
         const bool tu = p.r_max <= WL_TU_RMAX;
@@ -338,9 +379,30 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         ++t_launches;
         LeafArgs lb = la;
         lb.spill = nullptr; lb.spill_n = nullptr;
-        lb.list = spill_n + 1; lb.list_n = spill_n;
+        lb.list = status + 4; lb.list_n = spill_n;
         kern = wr ? k_leaf_wr32 : k_leaf_wor32;
         sm = sizeof(SLeaf<u32>);
+        const unsigned g2 = leaf_grid((const void *)kern, LEAF_NT, sm, 2ull * 148);
+        kern<<<g2, LEAF_NT, sm, st>>>(lb);
+        ++t_launches;
+        sp_leaf.end();
+        return cuda_ok();
+    } else if (wide && g_leaf_path != 1 && !p.gV) {
+        // wide leaf ranges: warp per leaf on 31-bit keys + payloads; the CTA
+        // kernel with 64-bit keys completes the leaves it spills (ties)
+        u32 *spill_n = status + 1;        // zeroed above
+        la.spill_n = spill_n;
+        la.spill = status + 4;
+        void (*wk)(LeafArgs) = wr ? k_leaf_warp_wide_wr : k_leaf_warp_wide_wor;
+        const size_t wsm = sizeof(WarpLeafW) * WL_WARPS;
+        const unsigned g1 = leaf_grid((const void *)wk, 32 * WL_WARPS, wsm, (p.nleaves + WL_WARPS - 1) / WL_WARPS);
+        wk<<<g1, 32 * WL_WARPS, wsm, st>>>(la);
+        ++t_launches;
+        LeafArgs lb = la;
+        lb.spill = nullptr; lb.spill_n = nullptr;
+        lb.list = status + 4; lb.list_n = spill_n;
+        kern = wr ? k_leaf_wr64 : k_leaf_wor64;
+        sm = sizeof(SLeaf<u64>);
         const unsigned g2 = leaf_grid((const void *)kern, LEAF_NT, sm, 2ull * 148);
         kern<<<g2, LEAF_NT, sm, st>>>(lb);
         ++t_launches;
@@ -611,7 +673,8 @@ __global__ void k_deviates_grp(int kind, u64 k, u64 L, u64 R, u64 seed, u64 id0,
 {
     const u64 ngrp = (u64)gridDim.x * blockDim.x / G;
     for (u64 i = (blockIdx.x * (u64)blockDim.x + threadIdx.x) / G; i < count; i += ngrp) {
-        const u64 x = kind ? binom_grp<G>(k, L, R, seed, id0 + i) : hgd_grp<G>(k, L, R, seed, id0 + i);
+        const u64 x = G == 32 ? (kind ? binom_tp(k, L, R, seed, id0 + i) : hgd_tp(k, L, R, seed, id0 + i))
+                              : (kind ? binom_grp<G>(k, L, R, seed, id0 + i) : hgd_grp<G>(k, L, R, seed, id0 + i));
         if ((threadIdx.x & (G - 1)) == 0) out[i] = x;
     }
 }
@@ -1051,6 +1114,10 @@ rs_status rs_set_option(int option, int value)
     }
     if (option == RS_OPT_TOPUP_MAX && value >= 0 && value <= 32) {
         g_topup_max = value;
+        return ret(RS_OK);
+    }
+    if (option == RS_OPT_SPLIT_COOP && (value == 0 || value == 1)) {
+        g_split_coop = value;
         return ret(RS_OK);
     }
     if (option == RS_OPT_LEAF_CAP && value >= 0 && value <= LEAF_CAP) {

@@ -1,6 +1,9 @@
 // rs_kernels.cu -- hot-path kernels of the B200 sampler (sm_100a).
 // P:n = /root/reference/PAPER.md line n; CANON readings R1-R12: DESIGN.md.
 #include "rs_kernels.cuh"
+#ifdef RS_SPLIT_PROF
+#include <cstdio>
+#endif
 
 namespace rs {
 
@@ -33,18 +36,32 @@ __device__ __forceinline__ void split_top(const SplitArgs &a)
     if (tid == 0) buf[0][0] = a.in_cnt ? a.in_cnt[blockIdx.x] : a.root_cnt;
     __syncthreads();
     int cur = 0;
+#ifdef RS_SPLIT_PROF
+    long long tl[16];
+    tl[0] = clock64();
+#endif
     for (int l = 0; l < a.nlev; ++l) {
+#ifdef RS_SPLIT_PROF
+        if (l) tl[l] = clock64();
+#endif
         const u32 width = 1u << l;
         const int d = a.ds + l;
         const u64 base = node << l;
         // narrow levels: a group of G lanes per node evaluates G rejection
         // iterations at once (hgd_grp), so a level costs ~one iteration's latency
-        if (width * 32 <= SPLIT_NT)     split_top_level<WR, 32>(a, buf[cur], buf[cur ^ 1], width, d, base);
+        // (a warp per node -- hgd_tp -- up to four nodes per warp)
+        if (width * 32 <= 4 * SPLIT_NT) split_top_level<WR, 32>(a, buf[cur], buf[cur ^ 1], width, d, base);
         else if (width * 8 <= SPLIT_NT) split_top_level<WR, 8>(a, buf[cur], buf[cur ^ 1], width, d, base);
         else                            split_top_level<WR, 1>(a, buf[cur], buf[cur ^ 1], width, d, base);
         __syncthreads();
         cur ^= 1;
     }
+#ifdef RS_SPLIT_PROF
+    if (tid == 0) {
+        tl[a.nlev] = clock64();
+        for (int l = 0; l < a.nlev; ++l) printf("split level %d: %lld cycles\n", l, tl[l + 1] - tl[l]);
+    }
+#endif
     // children's offsets: parent offset + exclusive scan of their counts
     const u32 W = 1u << a.nlev;
     const u32 per = (W + SPLIT_NT - 1) / SPLIT_NT;
@@ -128,6 +145,90 @@ __device__ __forceinline__ void split_deep(const LevelArgs &a)
     }
 }
 
+__device__ __forceinline__ u32 ld_acquire_u32(const u32 *p)
+{
+    u32 v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Grid-wide barrier of a cooperative launch: every CTA arrives once per level
+// (monotone counter); target = (level + 1) * gridDim.x.
+__device__ __forceinline__ void coop_barrier(u32 *bar, u32 target)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        while (ld_acquire_u32(bar) < target) __nanosleep(20);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <bool WR, int G>
+__device__ __forceinline__ void coop_level(const CoopArgs &a, int l, u64 width)
+{
+    const u32 tid = threadIdx.x;
+    const u64 ng = (u64)gridDim.x * COOP_NT / G;
+    const int d = a.ds + l;
+    const u64 base = a.node0 << l;
+    const u64 *icnt = a.buf_cnt[(l + 1) & 1], *ioff = a.buf_off[(l + 1) & 1];   // level l - 1's output
+    u64 *ocnt = a.buf_cnt[l & 1], *ooff = a.buf_off[l & 1];
+    const bool leaf = a.ds + l + 1 == a.D;
+    for (u64 j = ((u64)blockIdx.x * COOP_NT + tid) / G; j < width; j += ng) {
+        const u64 k = l ? __ldcg(icnt + j) : a.root_cnt;
+        const u64 off = l ? __ldcg(ioff + j) : 0;
+        const u64 x = split_node_grp<WR, G>(a.N, d, base + j, k, a.seed);
+        if ((tid & (G - 1)) == 0) {
+            if (leaf) {
+                if (k > 0xffffffffull) atomicOr(&g_rs_errors, 1u);
+                a.leaf_cnt[2 * j] = (u32)x;
+                a.leaf_cnt[2 * j + 1] = (u32)(k - x);
+                a.leaf_off[2 * j] = off;
+                a.leaf_off[2 * j + 1] = off + x;
+            } else {
+                ocnt[2 * j] = x;
+                ocnt[2 * j + 1] = k - x;
+                ooff[2 * j] = off;
+                ooff[2 * j + 1] = off + x;
+            }
+        }
+    }
+}
+
+template <bool WR>
+__device__ __forceinline__ void split_coop(const CoopArgs &a)
+{
+    const u64 nw = (u64)gridDim.x * (COOP_NT / 32);      // warps of the grid
+#ifdef RS_SPLIT_PROF
+    long long tw[24], tb[24];
+    long long t_prev = clock64();
+#endif
+    for (int l = 0; l < a.nlev; ++l) {
+        const u64 width = 1ull << l;
+        if (width <= 2 * nw)      coop_level<WR, 32>(a, l, width);
+        else if (width <= 8 * nw) coop_level<WR, 8>(a, l, width);
+        else                      coop_level<WR, 1>(a, l, width);
+#ifdef RS_SPLIT_PROF
+        const long long t_work = clock64();
+#endif
+        if (l + 1 < a.nlev) coop_barrier(a.bar, (u32)(l + 1) * gridDim.x);
+#ifdef RS_SPLIT_PROF
+        const long long t_bar = clock64();
+        if (l < 24) { tw[l] = t_work - t_prev; tb[l] = t_bar - t_work; }
+        t_prev = t_bar;
+#endif
+    }
+#ifdef RS_SPLIT_PROF
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        for (int l = 0; l < a.nlev && l < 24; ++l) printf("coop level %d: work %lld barrier %lld cycles\n", l, tw[l], tb[l]);
+#endif
+}
+
+__global__ void __launch_bounds__(COOP_NT, 1) k_split_coop(CoopArgs a) { split_coop<false>(a); }
+__global__ void __launch_bounds__(COOP_NT, 1) k_split_coop_wr(CoopArgs a) { split_coop<true>(a); }
+
 // WOR (hypergeometric) and WR (binomial) instantiations are separate
 // kernels: each holds only its deviate's code (the split kernels are
 // instruction-fetch bound).
@@ -151,6 +252,7 @@ __global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep4_wr(LevelArgs a) { s
 #include "rs_leaf.cuh"
 #include "rs_leaf_warp.cuh"
 #include "rs_leaf_lp.cuh"
+#include "rs_leaf_wide.cuh"
 #include "rs_leaf_bitmap.cuh"
 #include "rs_algb.cuh"
 
@@ -212,6 +314,26 @@ __device__ __forceinline__ u32 skip_fast64(u32 a, u32 b, double il, double m_abs
     const double rf = (double)r;
     ok = (lo >= rf && full) || (lo == hi && lo >= 0.0 && lo < rf);
     return lo >= rf ? r : (u32)fmin(fmax(lo, 0.0), rf);
+}
+
+// The u16 path's candidate (chunk ranges <= 2^16, rho >= 2^-6) from 32 bits
+// of the draw: U' = w 2^-32 with w = a when a >= 2^24 (b lies below fp32
+// precision there), else U' = w 2^-40 with w = (a << 8) | (b >> 24); in both
+// cases U' is within a relative 2^-23 of CANON's u52(a, b) (truncation 2^-24
+// plus the I2FP rounding 2^-24), inside the margin of skip_fast (whose
+// 2^-19 / |lr| term covers relative errors of U up to 2^-19).  32-bit I2FP
+// replaces the 64-bit I2F.  a < 2^16 (p = 2^-16) is left to the exact path.
+__device__ __forceinline__ u32 skip_fast16(u32 a, u32 b, float c, float m_abs, u32 r, bool &ok)
+{
+    const bool big = a >= (1u << 24);
+    const u32 w = big ? a : __funnelshift_l(b, a, 8);
+    const float U = __uint2float_rn(w) * (big ? 0x1p-32f : 0x1p-40f);
+    const float q = __log2f(U) * c;                                 // ~ log(U) / lr  (> 0)
+    const float mg = m_abs + q * 0x1p-20f;
+    const float lo = floorf(q - mg), hi = floorf(q + mg);
+    const float rf = (float)r;
+    ok = a >= (1u << 16) && (lo >= rf || lo == hi);                 // (lo == hi implies lo >= 0: q > 0)
+    return lo >= rf ? r : (u32)lo;
 }
 
 struct SkipParams {
@@ -280,10 +402,18 @@ __device__ __forceinline__ u32 bern_ticket(const BernArgs &a, u64 tk, B *bw, u32
             const u32x4 w0 = philox_rk(2 * (q0 + lane), st, a.rk);
             const u32x4 w1 = philox_rk(2 * (q0 + lane) + 1, st, a.rk);
             bool ok0, ok1, ok2, ok3;
-            const u32 g0 = skip_cand<F64>(w0.x, w0.y, sp, r32, rfull, ok0);
-            const u32 g1 = skip_cand<F64>(w0.z, w0.w, sp, r32, rfull, ok1);
-            const u32 g2 = skip_cand<F64>(w1.x, w1.y, sp, r32, rfull, ok2);
-            const u32 g3 = skip_cand<F64>(w1.z, w1.w, sp, r32, rfull, ok3);
+            u32 g0, g1, g2, g3;
+            if (sizeof(B) == 2 && !F64) {          // chunk ranges <= 2^16
+                g0 = skip_fast16(w0.x, w0.y, sp.c, sp.m_abs, r32, ok0);
+                g1 = skip_fast16(w0.z, w0.w, sp.c, sp.m_abs, r32, ok1);
+                g2 = skip_fast16(w1.x, w1.y, sp.c, sp.m_abs, r32, ok2);
+                g3 = skip_fast16(w1.z, w1.w, sp.c, sp.m_abs, r32, ok3);
+            } else {
+                g0 = skip_cand<F64>(w0.x, w0.y, sp, r32, rfull, ok0);
+                g1 = skip_cand<F64>(w0.z, w0.w, sp, r32, rfull, ok1);
+                g2 = skip_cand<F64>(w1.x, w1.y, sp, r32, rfull, ok2);
+                g3 = skip_cand<F64>(w1.z, w1.w, sp, r32, rfull, ok3);
+            }
             T s0 = (T)g0 + 1, s1 = (T)g1 + 1, s2 = (T)g2 + 1, s3 = (T)g3 + 1;
             if (__any_sync(0xffffffffu, !(ok0 && ok1 && ok2 && ok3))) {   // rare: exact fp64 (CANON)
                 if (!ok0) s0 = skip_exact<T>(u52(w0.x, w0.y), a.log1m_rho, r);
@@ -315,11 +445,14 @@ __device__ __forceinline__ u32 bern_ticket(const BernArgs &a, u64 tk, B *bw, u32
                 if (S3 <= r) { if (j0 + 3 < room) bg[j0 + 3] = (B)(S3 - 1); else overflow = true; }
             }
             const T tot = __shfl_sync(0xffffffffu, incl, 31);
-            const u32 e = __popc(__ballot_sync(0xffffffffu, S0 <= r)) + __popc(__ballot_sync(0xffffffffu, S1 <= r)) +
-                          __popc(__ballot_sync(0xffffffffu, S2 <= r)) + __popc(__ballot_sync(0xffffffffu, S3 <= r));
-            count += e;
-            if (e < 128) break;
-            S += tot;
+            if (S + tot <= r) {                    // the whole batch lies in the chunk (common)
+                count += 128;
+                S += tot;
+                continue;
+            }
+            count += __popc(__ballot_sync(0xffffffffu, S0 <= r)) + __popc(__ballot_sync(0xffffffffu, S1 <= r)) +
+                     __popc(__ballot_sync(0xffffffffu, S2 <= r)) + __popc(__ballot_sync(0xffffffffu, S3 <= r));
+            break;
         }
         if (__any_sync(0xffffffffu, overflow)) count = min(count, room);
         cnt[g] = count;
@@ -362,20 +495,16 @@ __device__ __forceinline__ void bern_write(const BernArgs &a, u64 tk, const B *b
         const u32 h = (u32)(reinterpret_cast<uintptr_t>(a.out + o0) >> 3) & 3u;
         u64 *d0 = a.out + (o0 - h);
         const u32 ng = (u32)((h + lim + 3) >> 2);
+        const B *bh = bw + boff - (int)h;                 // chunk value 4q - h + t = bh[4q + t]
         for (u32 q = lane; q < ng; q += 32) {
             const int i0 = (int)(4 * q) - (int)h;
-            u64 v[4];
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const int i = i0 + t;
-                v[t] = (i >= 0 && (u64)i < lim) ? out_word_t<GR>(base + (u64)bw[boff + i], a.gV) : 0ull;
-            }
-            if (i0 >= 0 && (u64)(i0 + 4) <= lim) {
-                st_v4b(d0 + 4 * q, v[0], v[1], v[2], v[3]);
+            if (i0 >= 0 && (u64)(i0 + 4) <= lim) {        // full group (common): no per-value tests
+                st_v4b(d0 + 4 * q, base + (u64)bh[4 * q], base + (u64)bh[4 * q + 1], base + (u64)bh[4 * q + 2],
+                       base + (u64)bh[4 * q + 3]);
             } else {
 #pragma unroll
                 for (int t = 0; t < 4; ++t)
-                    if (i0 + t >= 0 && (u64)(i0 + t) < lim) d0[4 * q + t] = v[t];
+                    if (i0 + t >= 0 && (u64)(i0 + t) < lim) d0[4 * q + t] = base + (u64)bw[boff + i0 + t];
             }
         }
         off += n;

@@ -14,7 +14,10 @@ constexpr int SPLIT_NT = 512;                     // top CTA: narrow levels use 
 constexpr int SPLIT_LEVELS = 11;                 // levels expanded per split phase
 constexpr int SPLIT_WIDTH = 1 << SPLIT_LEVELS;   // nodes per CTA at the phase's last level
 
-constexpr int LEAF_NT = 512;                     // threads per leaf CTA
+#ifndef RS_LEAF_NT
+#define RS_LEAF_NT 512
+#endif
+constexpr int LEAF_NT = RS_LEAF_NT;              // threads per leaf CTA
 #ifndef RS_LEAF_MINB
 #define RS_LEAF_MINB 2      // 2 CTAs per SM (64 registers): wide leaves 15 % faster
 #endif
@@ -90,9 +93,34 @@ struct SplitArgs {
 __global__ void __launch_bounds__(SPLIT_NT) k_split(SplitArgs a);
 __global__ void __launch_bounds__(SPLIT_NT) k_split_wr(SplitArgs a);
 
+// The narrow top of the tree in ONE cooperative launch (a CTA per SM, grid
+// barrier between levels): each level's nodes are spread over the grid's
+// warps -- a warp per node (hgd_tp) while there are few nodes, then 8-lane
+// groups, then a thread per node -- so a level costs about one deviate's
+// latency plus a barrier, with no launch or cold instruction cache per level.
+#ifndef RS_COOP_NT
+#define RS_COOP_NT 256
+#endif
+constexpr int COOP_NT = RS_COOP_NT;          // (256: up to 255 registers -- the deviates spill at 128)
+struct CoopArgs {
+    u64 N, seed;
+    int ds, nlev, D;                 // levels ds .. ds + nlev - 1 are split here
+    u64 node0;                       // subtree root index at depth ds
+    u64 root_cnt;
+    u64 *buf_cnt[2], *buf_off[2];    // level outputs alternate (ping, pong)
+    u32 *leaf_cnt;                   // ds + nlev == D: the leaf level's u32 counts + u64 offsets
+    u64 *leaf_off;
+    u32 *bar;                        // grid barrier counter (zeroed by the call)
+};
+__global__ void __launch_bounds__(COOP_NT, 1) k_split_coop(CoopArgs a);
+__global__ void __launch_bounds__(COOP_NT, 1) k_split_coop_wr(CoopArgs a);
+
 // One tree level across the whole GPU: thread j splits node (d, node0 + j).
 constexpr int LEVEL_NT = 128;
-constexpr int SPLIT_TOP = 10;                    // levels expanded by the single top CTA
+#ifndef RS_SPLIT_TOP
+#define RS_SPLIT_TOP 7
+#endif
+constexpr int SPLIT_TOP = RS_SPLIT_TOP;          // levels expanded by the single top CTA (then level kernels)
 struct LevelArgs {
     u64 N, seed;
     int wr, d;
@@ -177,6 +205,9 @@ __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr(Leaf
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm_tu(LeafArgs a);
+// wide leaf ranges (> 2^32 - 4096): 31-bit keys + payload (rs_leaf_wide.cuh)
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wide_wor(LeafArgs a);
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wide_wr(LeafArgs a);
 // Ordered linear-probing leaf kernels (rs_leaf_lp.cuh): the default WOR / WR path.
 #ifndef RS_LP_WARPS
 #define RS_LP_WARPS 16

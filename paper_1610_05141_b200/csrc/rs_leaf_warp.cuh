@@ -172,6 +172,8 @@ __device__ __forceinline__ u32 warp_excl_scan(u32 v, u32 lane)
     return incl - v;
 }
 
+__device__ __forceinline__ u32 wl_scan(WarpLeaf &sh, u32 lane);
+
 // Steps 1-2: count the round's J draws per bucket and stage them in draw
 // order at keys[0..J); scan the counts into starts.  Returns the largest
 // bucket load (0 if a bucket is a single value).
@@ -256,6 +258,17 @@ __device__ __forceinline__ u32 wl_count(WarpLeaf &sh, const RoundKeys &K, const 
 #endif
     __syncwarp();
     RS_TS(tc1);
+    const u32 P = wl_scan(sh, lane);
+    RS_TS(tc2);
+    RS_ACC(0, tc0, tc1);
+    RS_ACC(1, tc1, tc2);
+    return shb == 0 ? 0u : P;
+}
+
+// Step 2: scan the 1024 bucket counts (lane l owns buckets [32 l, 32 l + 32)
+// at words 33 l + i: conflict-free) into starts; returns the largest load.
+__device__ __forceinline__ u32 wl_scan(WarpLeaf &sh, u32 lane)
+{
     u32 *cl = sh.cnt + 33 * lane;
     u32 c[32];
 #pragma unroll
@@ -279,10 +292,7 @@ __device__ __forceinline__ u32 wl_count(WarpLeaf &sh, const RoundKeys &K, const 
         for (int g = 0; g < 4; ++g) { cl[8 * g + i] = rg[g]; rg[g] += c[8 * g + i]; }
     }
     __syncwarp();
-    RS_TS(tc2);
-    RS_ACC(0, tc0, tc1);
-    RS_ACC(1, tc1, tc2);
-    return shb == 0 ? 0u : P;
+    return P;
 }
 
 #ifndef RS_WL_REG

@@ -1,5 +1,6 @@
 """profiles/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum (bytes per
-launch) of each workload's dominant kernel, from the ncu --set full captures
+launch) and smsp__inst_executed.sum (warp instructions per launch, for
+roofline.issue) of each workload's dominant kernel, from the ncu --set full captures
 gpurun_out/full_<workload>.ncu-rep (read by bench.py for roofline.traffic)."""
 import csv
 import json
@@ -29,6 +30,8 @@ for w in ["headline", "cfg1", "complement", "wr", "bernoulli", "gnm", "algb"]:
         i = h.index(name)
         tot += float(v[i].replace(",", "")) * UNIT[u[i]]
     name = bench._workload(w, 1)["name"]
-    out[name] = {"bytes_per_launch": tot, "kernel": v[h.index("Kernel Name")], "source": f"full_{w}.ncu-rep"}
+    wi = float(v[h.index("smsp__inst_executed.sum")].replace(",", "")) if "smsp__inst_executed.sum" in h else None
+    out[name] = {"bytes_per_launch": tot, "warp_inst_per_launch": wi, "kernel": v[h.index("Kernel Name")],
+                 "source": f"full_{w}.ncu-rep"}
     print(name, out[name])
 json.dump(out, open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
