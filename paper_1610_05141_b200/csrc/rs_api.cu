@@ -21,6 +21,12 @@ int g_leaf_path = 0;                    // rs_set_option(RS_OPT_LEAF_PATH)
 int g_topup_max = 32;                   // rs_set_option(RS_OPT_TOPUP_MAX)
 int g_leaf_cap = 0;                     // rs_set_option(RS_OPT_LEAF_CAP) (tests: force overflows)
 int g_split_coop = 1;                   // rs_set_option(RS_OPT_SPLIT_COOP): cooperative top of the split tree
+#ifndef RS_WL_P2
+#define RS_WL_P2 1
+#endif
+#ifndef RS_WL_P2_PLAIN
+#define RS_WL_P2_PLAIN 0        // 1: large power-of-two ranges take the plain (no top-up) p2 kernel
+#endif
 #ifndef RS_COOP_LEVELS
 #define RS_COOP_LEVELS 15               // input widths 1 .. 2^14
 #endif
@@ -368,9 +374,15 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
             const unsigned gl = leaf_grid((const void *)lk, 32 * LP_WARPS, lsm, (p.nleaves + LP_WARPS - 1) / LP_WARPS);
             lk<<<gl, 32 * LP_WARPS, lsm, st>>>(la);
         } else {
-            void (*wk)(LeafArgs) = wr ? k_leaf_warp_wr
+            // N a power of two: every leaf range is one (r = N / 2^D) -> the
+            // kernels compiled without the Lemire rejection path
+            const bool p2 = (p.N & (p.N - 1)) == 0 && RS_WL_P2;
+            void (*wk)(LeafArgs) = wr ? (p2 ? k_leaf_warp_wr_p2 : k_leaf_warp_wr)
                                  : p.gV ? (tu ? k_leaf_warp_gnm_tu : k_leaf_warp_gnm)
-                                        : ((tu || RS_WL_WOR_TU_ALL) ? k_leaf_warp_wor_tu : k_leaf_warp_wor);
+                                        : ((tu || RS_WL_WOR_TU_ALL)
+                                               ? (p2 ? (!tu && RS_WL_P2_PLAIN ? k_leaf_warp_wor_p2 : k_leaf_warp_wor_tu_p2)
+                                                     : k_leaf_warp_wor_tu)
+                                               : k_leaf_warp_wor);
             const size_t wsm = sizeof(WarpLeaf) * WL_WARPS;
             const u64 wgrid = (p.nleaves + WL_WARPS - 1) / WL_WARPS;
             const unsigned g1 = leaf_grid((const void *)wk, 32 * WL_WARPS, wsm, wgrid);

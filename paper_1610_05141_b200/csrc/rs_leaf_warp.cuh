@@ -128,12 +128,13 @@ struct WDrawer {
         }
         v[0] = shr32(c0, s); v[1] = shr32(c1, s); v[2] = shr32(c2, s); v[3] = shr32(c3, s);
     }
+    template <bool P2 = false>
     __device__ __forceinline__ void block(const RoundKeys &K, u32 q, u32 *v) const
     {
 #ifdef RS_EXP_NOPHILOX
         { const u32 t = q * 0x9E3779B9u ^ d.st.id_lo; v[0] = shr32(t, s); v[1] = shr32(t * 3u, s); v[2] = shr32(t * 5u, s); v[3] = shr32(t * 7u, s); return; }
 #endif
-        if (pow2) {
+        if (P2 || pow2) {          // P2: every leaf range of the launch is a power of two
             u32 c0 = q, c1 = d.st.tag, c2 = d.st.id_lo, c3 = d.st.id_hi;
 #pragma unroll
             for (int r = 0; r < 10; ++r) {
@@ -177,6 +178,7 @@ __device__ __forceinline__ u32 wl_scan(WarpLeaf &sh, u32 lane);
 // Steps 1-2: count the round's J draws per bucket and stage them in draw
 // order at keys[0..J); scan the counts into starts.  Returns the largest
 // bucket load (0 if a bucket is a single value).
+template <bool P2>
 __device__ __forceinline__ u32 wl_count(WarpLeaf &sh, const RoundKeys &K, const WDrawer &dr, u32 J, int shb, u32 lane)
 {
     RS_TS(tc0);
@@ -188,7 +190,7 @@ __device__ __forceinline__ u32 wl_count(WarpLeaf &sh, const RoundKeys &K, const 
     for (u32 q0 = lane; q0 < nq; q0 += 32 * RS_WL_CB) {
         u32 v[RS_WL_CB][4];
 #pragma unroll
-        for (int c = 0; c < RS_WL_CB; ++c) dr.block(K, q0 + 32 * c, v[c]);
+        for (int c = 0; c < RS_WL_CB; ++c) dr.block<P2>(K, q0 + 32 * c, v[c]);
         if (q0 + 32 * (RS_WL_CB - 1) < qfull) {
 #pragma unroll
             for (int w = 0; w < 4; ++w)
@@ -211,8 +213,8 @@ __device__ __forceinline__ u32 wl_count(WarpLeaf &sh, const RoundKeys &K, const 
     for (u32 q = lane; q < nq; q += 64) {        // two independent Philox blocks per step (ILP)
         const u32 q2 = q + 32;
         u32 v[4], v2[4];
-        dr.block(K, q, v);
-        dr.block(K, q2, v2);
+        dr.block<P2>(K, q, v);
+        dr.block<P2>(K, q2, v2);
 #if RS_WL_RANK && !defined(RS_WL_REGEN)
         // ATOMS with return: the old count is the draw's rank in its bucket
         // (ranks above 255 wrap, but then the bucket load exceeds WL_PMAX and
@@ -523,7 +525,7 @@ __device__ __noinline__ void wl_store_edges(const WarpLeaf &sh, u64 *d0, u32 h, 
 // moves up by the number of new values below it).  Up to 32 new values (one
 // per lane; at most LeafArgs::topup_max); more returns false and the caller
 // runs the full round.
-template <bool GR>
+template <bool GR, bool P2>
 __device__ __forceinline__ bool wl_topup(const WarpLeaf &sh, const RoundKeys &K, const WDrawer &dr, u32 J, u32 k,
                                       u32 dist, u32 h, u64 base, u64 *d0, u32 lane, u64 gV, u32 tmax)
 {
@@ -534,7 +536,7 @@ __device__ __forceinline__ bool wl_topup(const WarpLeaf &sh, const RoundKeys &K,
     u32 nv = 0, mv = 0xffffffffu, mr = 0;            // lane t < nv: t-th new value and its rank in ks
     for (u32 j0 = J; nv < need; j0 += 32) {
         u32 v[4];
-        dr.block(K, (j0 + lane) >> 2, v);
+        dr.block<P2>(K, (j0 + lane) >> 2, v);
         const u32 w = (j0 + lane) & 3u;
         const u32 xl = w == 0 ? v[0] : w == 1 ? v[1] : w == 2 ? v[2] : v[3];
         for (u32 t = 0; t < 32 && nv < need; ++t) {
@@ -778,7 +780,7 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
     return 0;
 }
 
-template <bool WR, bool GR, bool TU>
+template <bool WR, bool GR, bool TU, bool P2 = false>
 __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -843,7 +845,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
             }
 #else
             if (J + h <= (u32)WL_CAP) {
-                const u32 P = wl_count(sh, a.rk, dr, J, shb, lane);
+                const u32 P = wl_count<P2>(sh, a.rk, dr, J, shb, lane);
                 if (P > WL_PMAX) {              // pathological bucket load
                     wl_clear(sh, lane);
                     __syncwarp();
@@ -873,7 +875,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
             }
             if (TU && (res & WL_TOPUP)) {       // |S| < k: top up draw by draw, else a full round
                 const u32 dist = res & ~WL_TOPUP;
-                if (wl_topup<GR>(sh, a.rk, dr, J, k, dist, h, base, dst - h, lane, a.gV, a.topup_max)) break;
+                if (wl_topup<GR, P2>(sh, a.rk, dr, J, k, dist, h, base, dst - h, lane, a.gV, a.topup_max)) break;
                 res = J + (k - dist);
             }
             J = res;
@@ -888,5 +890,9 @@ __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu(
 // G(n, m) (NEXT-3): the WOR kernel with the edge decode fused into its stores
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm(LeafArgs a) { warp_leaves<false, true, false>(a); }
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm_tu(LeafArgs a) { warp_leaves<false, true, true>(a); }
+// every leaf range a power of two (N = 2^a): no Lemire rejection code at all
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu_p2(LeafArgs a) { warp_leaves<false, false, true, true>(a); }
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr_p2(LeafArgs a) { warp_leaves<true, false, false, true>(a); }
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_p2(LeafArgs a) { warp_leaves<false, false, false, true>(a); }
 
 }  // namespace rs
