@@ -38,6 +38,10 @@ __global__ void k_lat(u64 *out, long long *cyc, double xin)
     t0 = clock64();
     for (int i = 0; i < 8; ++i) X += hgd_tp(k, L, R, 1 + X % 3, 1 + i);
     t1 = clock64(); cyc[5] = (t1 - t0) / 8;
+    // 6b. hgd_tp on cfg0-shaped nodes (k = 2^20 >> l, R = 2^30 >> l)
+    t0 = clock64();
+    for (int l = 0; l < 10; ++l) X += hgd_tp((1ull << 20) >> l, (1ull << 29) >> l, (1ull << 30) >> l, 1 + X % 3, (1ull << l));
+    t1 = clock64(); cyc[7] = (t1 - t0) / 10;
     // 7. hrua_setup
     t0 = clock64();
     Hrua s;
@@ -52,9 +56,9 @@ int main()
     cudaMalloc(&o, 8); cudaMalloc(&c, 64 * 8);
     for (int rep = 0; rep < 3; ++rep) k_lat<<<1, 32>>>(o, c, 0.5);
     cudaDeviceSynchronize();
-    long long h[8];
-    cudaMemcpy(h, c, 7 * 8, cudaMemcpyDeviceToHost);
-    const char *nm[] = {"fp64 div (dependent)", "log_", "stirlerr", "log_dbinom", "hgd (1 lane)", "hgd_tp (32 lanes)", "hrua_setup"};
-    for (int i = 0; i < 7; ++i) printf("%-24s %8lld cycles\n", nm[i], h[i]);
+    long long h[8] = {0};
+    cudaMemcpy(h, c, 8 * 8, cudaMemcpyDeviceToHost);
+    const char *nm[] = {"fp64 div (dependent)", "log_", "stirlerr", "log_dbinom", "hgd (1 lane)", "hgd_tp (32 lanes)", "hrua_setup", "hgd_tp cfg0 nodes"};
+    for (int i = 0; i < 8; ++i) printf("%-24s %8lld cycles\n", nm[i], h[i]);
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
 }
