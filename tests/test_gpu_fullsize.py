@@ -49,29 +49,33 @@ def _wor_digest(N, n, seed, mode):
     return d
 
 
-@pytest.mark.parametrize("cfg,seed", [("HEADLINE", 1)] + [("CFG1", s) for s in W.PARITY_SEEDS])
+@pytest.mark.parametrize("cfg,seed", [("HEADLINE", 1), ("HEADLINE", 2 ** 64 - 1)] +
+                         [("CFG1", s) for s in W.PARITY_SEEDS])
 def test_fullsize_wor_digest(cfg, seed):
     c = getattr(W, cfg)
     N, n = c["N"], c["n"]
     assert _wor_digest(N, n, seed, O.MODE_WOR) == O.digest_range(N, n, seed, O.MODE_WOR)
 
 
-def test_fullsize_complement_digest():
+@pytest.mark.parametrize("seed", W.PARITY_SEEDS)
+def test_fullsize_complement_digest(seed):
     c = W.CFG3A
-    N, n, seed = c["N"], c["n"], c["seed"]
+    N, n = c["N"], c["n"]
     assert _wor_digest(N, n, seed, O.MODE_WOR) == O.digest_range(N, n, seed, O.MODE_WOR)
 
 
-def test_fullsize_wr_digest():
+@pytest.mark.parametrize("seed", [1, 2 ** 64 - 1])
+def test_fullsize_wr_digest(seed):
     c = W.CFG4
-    N, n, seed = c["N"], c["n"], c["seed"]
+    N, n = c["N"], c["n"]
     assert _wor_digest(N, n, seed, O.MODE_WR) == O.digest_range(N, n, seed, O.MODE_WR)
 
 
-@pytest.mark.parametrize("cfg", ["CFG3B", "CFG3B_ROOF"])
-def test_fullsize_bernoulli_digest(cfg):
+@pytest.mark.parametrize("cfg,seed", [("CFG3B", s) for s in W.PARITY_SEEDS] +
+                         [("CFG3B_ROOF", 1), ("CFG3B_ROOF", 2 ** 64 - 1)])
+def test_fullsize_bernoulli_digest(cfg, seed):
     c = getattr(W, cfg)
-    N, rho, seed = c["N"], c["rho"], c["seed"]
+    N, rho = c["N"], c["rho"]
     out = rs.bernoulli(N, rho, seed)
     torch.cuda.synchronize()
     d_gpu, cnt = rs.digest(out), out.numel()

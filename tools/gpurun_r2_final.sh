@@ -17,9 +17,16 @@ python bench.py --steps 2 --warmup 1 --launch-list --no-e2e --no-cpu > gpurun_ou
 for spec in headline:k_leaf_warp_wor_tu_p2 cfg1:k_leaf_warp_wor_tu_p2 wr:k_leaf_warp_wr_p2 complement:k_leaf_bitmap_comp bernoulli:k_bernoulli headline:k_split_deep3 cfg0:k_split_coop gnm:k_leaf_warp_gnm algb:k_bernoulli64d; do
   W=${spec%%:*}; K=${spec#*:}
   timeout 300 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --workload $W > gpurun_out/r2_plain_$W.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$K" -s 1 -c 1 -o gpurun_out/r2_full_${W}_${K} -f \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$K" -s 1 -c 1 -o /tmp/r2_full_${W}_${K} -f \
       python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --workload $W > gpurun_out/r2_ncu_${W}_${K}.log 2>&1
   echo "$W $K ncu rc=$?" >> gpurun_out/r2_box.txt
+  # export here (the reports are too large to bring back): details, raw, per-line source
+  R=/tmp/r2_full_${W}_${K}.ncu-rep
+  ncu -i $R --page details --csv > gpurun_out/r2_full_${W}_${K}_details.csv 2>/dev/null
+  ncu -i $R --page raw --csv > gpurun_out/r2_full_${W}_${K}_raw.csv 2>/dev/null
+  ncu -i $R --page source --csv --print-source cuda,sass > gpurun_out/r2_full_${W}_${K}_source.csv 2>/dev/null
+  gzip -f gpurun_out/r2_full_${W}_${K}_source.csv
+  if [ "$W" = headline ] && [ "$K" = k_leaf_warp_wor_tu_p2 ]; then cp $R gpurun_out/; fi
 done
 timeout 600 python tools/sweep.py > gpurun_out/r2_sweep.txt 2>&1
 ./tools/ubench/ubench > gpurun_out/r2_ubench.txt 2>&1

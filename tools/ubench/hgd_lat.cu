@@ -50,6 +50,69 @@ __global__ void k_lat(u64 *out, long long *cyc, double xin)
     if (threadIdx.x == 0) out[0] = X + (u64)acc;
 }
 
+
+__device__ long long g_ph[8];
+__device__ __noinline__ u64 hgd_tp_timed(u64 k, u64 L, u64 R, u64 seed, u64 node_id)
+{
+    long long t0 = clock64();
+    const u64 kp = (R - k) < k ? R - k : k;
+    const u64 g = (R - L) < L ? R - L : L;
+    const Stream st(seed, P_HGD, node_id);
+    const u32 lane = threadIdx.x & 31;
+    const double p = (double)g / (double)R;
+    const double q = (double)(R - g) / (double)R;
+    const double a = (double)kp * p + 0.5;
+    const double var = (double)(R - kp) * (double)kp * p * q / (double)(R - 1);
+    const double c = sqrt_(var + 0.5);
+    const double h = 0x1.b72cd3f331398p+0 * c + 0x1.cc3ebd3bc711ap-1;
+    const unsigned __int128 num = (unsigned __int128)(kp + 1) * (unsigned __int128)(g + 1);
+    const u64 den = R + 2;
+    u64 M = (u64)(((double)(kp + 1) * (double)(g + 1)) / (double)den);
+    while ((unsigned __int128)M * den > num) --M;
+    while ((unsigned __int128)(M + 1) * den <= num) ++M;
+    const double cap = (double)(kp < g ? kp : g) + 1.0;
+    const double tail = floor_(a + 16 * c);
+    const double b = cap < tail ? cap : tail;
+    long long t1 = clock64();
+    const HgdCore core{kp, g, R, (double)kp / (double)R, (double)(R - kp) / (double)R,
+                       stirlerr((double)g), stirlerr((double)(R - g))};
+    long long t2 = clock64();
+    const u32 first = 2u;
+    const bool mode_lane = lane < first;
+    const u32 j = mode_lane ? 0u : (lane - first) >> 1, half = (lane - first) & 1;
+    const u32x4 w = st.block(j);
+    const double U = u52(w.x, w.y), V = u52(w.z, w.w);
+    const double Xc = a + h * (V - 0.5) / U;
+    const bool inb = !(Xc < 0.0 || Xc >= b);
+    const u64 K = mode_lane ? M : (inb ? (u64)floor_(Xc) : M);
+    long long t3 = clock64();
+    const u32 hh = mode_lane ? lane : half;
+    const double val = hh == 0 ? log_dbinom((double)K, (double)g, core.pp, core.qq, core.sg)
+                               : log_dbinom((double)(kp - K), (double)(R - g), core.pp, core.qq, core.sr);
+    long long t4 = clock64();
+    const double lu = half == 0 && !mode_lane ? log_(U) : 0.0;
+    long long t5 = clock64();
+    const double TM = __shfl_sync(0xffffffffu, val, 0) + __shfl_sync(0xffffffffu, val, 1);
+    const double d1 = __shfl_down_sync(0xffffffffu, val, 1);
+    bool acc = false;
+    if (!mode_lane && half == 0 && inb) {
+        const double T = val + d1 - TM;
+        if (U * (4.0 - U) - 3.0 <= T) acc = true;
+        else if (!(U * (U - T) >= 1.0)) acc = 2.0 * lu <= T;
+    }
+    const u32 am = __ballot_sync(0xffffffffu, acc);
+    u64 X = am ? __shfl_sync(0xffffffffu, K, __ffs(am) - 1) : 0;
+    long long t6 = clock64();
+    if (lane == 0) { g_ph[0] = t1 - t0; g_ph[1] = t2 - t1; g_ph[2] = t3 - t2; g_ph[3] = t4 - t3; g_ph[4] = t5 - t4; g_ph[5] = t6 - t5; }
+    return X;
+}
+__global__ void k_phases(u64 *out)
+{
+    u64 X = 0;
+    for (int i = 0; i < 4; ++i) X += hgd_tp_timed(1ull << 20, 1ull << 29, 1ull << 30, 1 + i, 1 + i);
+    if (threadIdx.x == 0) out[0] = X;
+}
+
 int main()
 {
     u64 *o; long long *c;
@@ -60,5 +123,11 @@ int main()
     cudaMemcpy(h, c, 8 * 8, cudaMemcpyDeviceToHost);
     const char *nm[] = {"fp64 div (dependent)", "log_", "stirlerr", "log_dbinom", "hgd (1 lane)", "hgd_tp (32 lanes)", "hrua_setup", "hgd_tp cfg0 nodes"};
     for (int i = 0; i < 8; ++i) printf("%-24s %8lld cycles\n", nm[i], h[i]);
+    k_phases<<<1, 32>>>(o);
+    cudaDeviceSynchronize();
+    long long ph[8];
+    cudaMemcpyFromSymbol(ph, g_ph, 8 * 8);
+    const char *pn[] = {"setup (p,q,a,var,sqrt,M,b)", "stirlerr(g), stirlerr(R-g)", "Philox + candidate", "log_dbinom (lane)", "log_(U)", "gather + decide"};
+    for (int i = 0; i < 6; ++i) printf("hgd_tp phase %-28s %8lld cycles\n", pn[i], ph[i]);
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
 }
