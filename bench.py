@@ -400,11 +400,15 @@ def run_native(args):
         r_max = (N >> D) + 1
         if mode == "wor" and r_max <= 2 ** 15:
             kname = "k_leaf_bitmap_comp" if comp else "k_leaf_bitmap_wor"
+        elif r_max > 0xfffff000 and mode != "gnm":
+            kname = "k_leaf_warp_wide_wr" if mode == "wr" else "k_leaf_warp_wide_wor"
         else:
             kname = {"wr": "k_leaf_warp_wr", "gnm": "k_leaf_warp_gnm"}.get(mode, "k_leaf_warp_wor")
             # the top-up kernels: plain WOR at every range, G(n, m) for small ranges
             if mode == "wor" or (mode == "gnm" and r_max <= 2 ** 21):
                 kname += "_tu"
+            if mode in ("wor", "wr") and (N & (N - 1)) == 0:     # power-of-two N: the _p2 kernels
+                kname += "_p2"
     kms_per = kms / max(kl, 1)
     achieved = bytes_per_launch / (kms_per / 1e3) / 1e9 if kms_per > 0 else None
     traffic, winst = None, None
