@@ -298,7 +298,10 @@ __device__ __forceinline__ u32 wl_scan(WarpLeaf &sh, u32 lane)
 }
 
 #ifndef RS_WL_REG
-#define RS_WL_REG 0         // 1: draws stay in registers from the count to the scatter (no staging round trip)
+#define RS_WL_REG 0         // 1: draws stay in registers from the count to the scatter (no staging round trip) in every kernel
+#endif
+#ifndef RS_WL_REG_P2
+#define RS_WL_REG_P2 1      // ... in the power-of-two WOR kernels only (spill-free there)
 #endif
 
 // Monotone bucket of a draw x < 2^cr (cr >= 11), 1056 buckets:
@@ -825,16 +828,18 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
 #endif
         constexpr bool SMST = RS_WL_SMEMST || (RS_WL_SMEMST_GR && GR);
         u32 J = k;
-#if RS_WL_REG
-        const u32 M = wl_bucket_mult(cr);
-#endif
+        // the register-resident count/scatter: for the power-of-two WOR kernels
+        // (no spills there; measured headline 12.45 -> 12.26 ms, cfg1 4.64 ->
+        // 4.33) or everywhere with RS_WL_REG (spills elsewhere; WR slower)
+        constexpr bool REG = RS_WL_REG || (RS_WL_REG_P2 && P2 && !WR && !GR);
+        const u32 M = REG ? wl_bucket_mult(cr) : 0u;
         for (;;) {
             u32 res = 0xffffffffu;
-#if RS_WL_REG
+            if (REG) {
             if (J + h <= (u32)WL_CAP) {
                 u32 x[WL_E1];
-                const u32 P = dr.pow2 ? wl_count_reg<true>(sh, a.rk, dr, J, M, lane, x)
-                                      : wl_count_reg<false>(sh, a.rk, dr, J, M, lane, x);
+                const u32 P = (P2 || dr.pow2) ? wl_count_reg<true>(sh, a.rk, dr, J, M, lane, x)
+                                              : wl_count_reg<false>(sh, a.rk, dr, J, M, lane, x);
                 if (P > WL_PMAX) {              // pathological bucket load
                     wl_clear(sh, lane);
                     __syncwarp();
@@ -843,7 +848,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
                     res = wl_finish<WL_E1, WR, GR, TU>(sh, J, k, h, P, SMST ? 0 : base, SMST ? nullptr : dst, lane, a.gV);
                 }
             }
-#else
+            } else {
             if (J + h <= (u32)WL_CAP) {
                 const u32 P = wl_count<P2>(sh, a.rk, dr, J, shb, lane);
                 if (P > WL_PMAX) {              // pathological bucket load
@@ -867,7 +872,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
 #endif
                 }
             }
-#endif
+            }
             if (res == 0) break;
             if (res == 0xffffffffu) {           // the CTA kernel completes this leaf
                 if (lane == 0) a.spill[atomicAdd(a.spill_n, 1u)] = (u32)L;
