@@ -268,9 +268,14 @@ rs_status rs_device_errors(int clear, unsigned *flags);
  * RS_OPT_LEAF_CAP: 0 (default) or 1..2048, the CTA leaf kernel's draw
  * capacity; small values force capacity overflows so that tests can check
  * that they are reported (RS_ECAPACITY from the checked calls).
- * Results are identical for every setting of the first two (the third
- * changes which leaves fail).  Unknown option or value -> RS_EINVAL. */
-enum { RS_OPT_LEAF_PATH = 1, RS_OPT_TOPUP_MAX = 2, RS_OPT_LEAF_CAP = 3, RS_OPT_SPLIT_COOP = 4 };
+ * RS_OPT_FUSED: 1 (default) = trees of <= 2^11 leaves (the shard's depth
+ * D - s <= 11) on the warp-leaf paths run split and leaves in one launch,
+ * each CTA walking the path from the shard root to its 16-leaf subtree
+ * (n up to ~2^21; rs_fused.cuh); 0 = the separate split and leaf launches.
+ * Results are identical for every setting of LEAF_PATH, TOPUP_MAX,
+ * SPLIT_COOP and FUSED (LEAF_CAP changes which leaves fail).  Unknown option
+ * or value -> RS_EINVAL. */
+enum { RS_OPT_LEAF_PATH = 1, RS_OPT_TOPUP_MAX = 2, RS_OPT_LEAF_CAP = 3, RS_OPT_SPLIT_COOP = 4, RS_OPT_FUSED = 5 };
 rs_status rs_set_option(int option, int value);
 
 /* Number of kernel launches issued by this thread since the last reset. */

@@ -15,7 +15,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librs.so")
 SOURCES = ["librs.cu", "rs_api.cu", "rs_kernels.cu", "rs_kernels.cuh", "rs_math.cuh", "rs_leaf.cuh",
-           "rs_leaf_warp.cuh", "rs_leaf_lp.cuh", "rs_leaf_wide.cuh", "rs_leaf_bitmap.cuh", "rs_algb.cuh"]
+           "rs_leaf_warp.cuh", "rs_leaf_lp.cuh", "rs_leaf_wide.cuh", "rs_leaf_bitmap.cuh", "rs_algb.cuh",
+           "rs_fused.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -21,6 +21,10 @@ int g_leaf_path = 0;                    // rs_set_option(RS_OPT_LEAF_PATH)
 int g_topup_max = 32;                   // rs_set_option(RS_OPT_TOPUP_MAX)
 int g_leaf_cap = 0;                     // rs_set_option(RS_OPT_LEAF_CAP) (tests: force overflows)
 int g_split_coop = 1;                   // rs_set_option(RS_OPT_SPLIT_COOP): cooperative top of the split tree
+int g_fused = 1;                        // rs_set_option(RS_OPT_FUSED): small trees in one launch (rs_fused.cuh)
+#ifndef RS_WL_WOR_TU_ALL
+#define RS_WL_WOR_TU_ALL 1
+#endif
 #ifndef RS_WL_P2
 #define RS_WL_P2 1
 #endif
@@ -205,6 +209,61 @@ unsigned leaf_grid(const void *kern, int threads, size_t smem, u64 work)
     return (unsigned)(work < g ? (work ? work : 1) : g);
 }
 
+// Small trees on the warp-leaf paths: the split and the leaves in one launch
+// (rs_fused.cuh), then the (usually empty) spill pass.  Returns false (nothing
+// launched) when the plan is not one.
+bool run_fused(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t st)
+{
+    const int depth = p.D - p.s;
+    if (!g_fused || depth < 0 || depth > RS_FUSED_MAXD || p.comp || p.gV || g_leaf_path != 0) return false;
+    const bool wr = (p.mode == RS_MODE_WR);
+    const bool wide = p.r_max > 0xfffff000ull;
+    if (p.r_max <= BM_RMAX && !wr) return false;                   // bitmap leaves
+    const bool w32 = !wide && (p.N >> p.D) >= (1ull << 11);
+    if (!w32 && !wide) return false;
+    const bool p2 = (p.N & (p.N - 1)) == 0 && RS_WL_P2;
+    const bool tu = p.r_max <= WL_TU_RMAX;
+    if (w32 && !wr && !(tu || RS_WL_WOR_TU_ALL)) return false;     // the plain WOR kernel
+    if (w32 && !wr && p2 && !tu && RS_WL_P2_PLAIN) return false;
+    u32 *status = (u32 *)(ws + p.o_spill);
+    u32 *leaf_cnt = (u32 *)(ws + p.o_leaf_cnt);
+    u64 *leaf_off = (u64 *)(ws + p.o_leaf_off);
+    FusedArgs f;
+    memset(&f, 0, sizeof f);
+    LeafArgs &la = f.la;
+    la.N = p.N; la.seed = p.seed; la.D = p.D;
+    la.leaf0 = p.leaf0; la.nleaves = p.nleaves;
+    la.cnt = leaf_cnt; la.off = leaf_off; la.out = out;
+    la.rk = round_keys(p.seed);
+    la.status = status;
+    la.cap = (u32)g_leaf_cap;
+    la.topup_max = (u32)g_topup_max;
+    la.spill_n = status + 1;
+    la.spill = status + 4;
+    f.N = p.N; f.seed = p.seed; f.s = p.s; f.D = p.D;
+    f.lb = depth < FUSED_LB ? depth : FUSED_LB;
+    f.idx = p.idx; f.root_cnt = p.root_cnt;
+    f.leaf_cnt = leaf_cnt; f.leaf_off = leaf_off;
+    void (*fk)(FusedArgs) = wide ? (wr ? k_fused_wide_wr : k_fused_wide_wor)
+                          : wr ? (p2 ? k_fused_wr_p2 : k_fused_wr)
+                               : (p2 ? k_fused_wor_tu_p2 : k_fused_wor_tu);
+    const size_t fsm = wide ? sizeof(WarpLeafW) * WL_WARPS : sizeof(WarpLeaf) * WL_WARPS;
+    (void)leaf_grid((const void *)fk, 32 * WL_WARPS, fsm, 1);      // (attributes)
+    Span sp(1, st);
+    fk<<<1u << (depth - f.lb), 32 * WL_WARPS, fsm, st>>>(f);
+    ++t_launches;
+    LeafArgs lb = la;
+    lb.spill = nullptr; lb.spill_n = nullptr;
+    lb.list = status + 4; lb.list_n = status + 1;
+    void (*kern)(LeafArgs) = wide ? (wr ? k_leaf_wr64 : k_leaf_wor64) : (wr ? k_leaf_wr32 : k_leaf_wor32);
+    const size_t sm = wide ? sizeof(SLeaf<u64>) : sizeof(SLeaf<u32>);
+    const unsigned g2 = leaf_grid((const void *)kern, LEAF_NT, sm, p.nleaves < 2ull * 148 ? p.nleaves : 2ull * 148);
+    kern<<<g2, LEAF_NT, sm, st>>>(lb);
+    ++t_launches;
+    sp.end();
+    return true;
+}
+
 // Launch the split phases and the leaf kernel of a tree plan.  The call's
 // status word (ws + o_spill) is zeroed here when clear_status is set;
 // otherwise it accumulates over several run_tree calls (host-buffer batches).
@@ -221,6 +280,7 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         cudaMemsetAsync(status, 0, 16, st);
     else
         cudaMemsetAsync(status + 1, 0, 12, st);
+    if (run_fused(p, out, ws, st)) return cuda_ok();
     u64 *ping_cnt = (u64 *)(ws + p.o_ping_cnt), *ping_off = (u64 *)(ws + p.o_ping_off);
     u64 *pong_cnt = (u64 *)(ws + p.o_pong_cnt), *pong_off = (u64 *)(ws + p.o_pong_off);
     u32 *leaf_cnt = (u32 *)(ws + p.o_leaf_cnt);
@@ -1130,6 +1190,10 @@ rs_status rs_set_option(int option, int value)
     }
     if (option == RS_OPT_SPLIT_COOP && (value == 0 || value == 1)) {
         g_split_coop = value;
+        return ret(RS_OK);
+    }
+    if (option == RS_OPT_FUSED && (value == 0 || value == 1)) {
+        g_fused = value;
         return ret(RS_OK);
     }
     if (option == RS_OPT_LEAF_CAP && value >= 0 && value <= LEAF_CAP) {

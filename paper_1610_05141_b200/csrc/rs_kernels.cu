@@ -253,6 +253,7 @@ __global__ void __launch_bounds__(LEVEL_NT, 4) k_split_deep4_wr(LevelArgs a) { s
 #include "rs_leaf_warp.cuh"
 #include "rs_leaf_lp.cuh"
 #include "rs_leaf_wide.cuh"
+#include "rs_fused.cuh"
 #include "rs_leaf_bitmap.cuh"
 #include "rs_algb.cuh"
 

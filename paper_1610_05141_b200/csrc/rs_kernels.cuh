@@ -211,6 +211,25 @@ __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_p2(
 // wide leaf ranges (> 2^32 - 4096): 31-bit keys + payload (rs_leaf_wide.cuh)
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wide_wor(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wide_wr(LeafArgs a);
+// Small trees: split + leaves in one launch (rs_fused.cuh); CTA c owns the
+// WL_WARPS leaves under node c at depth D - lb of the shard rooted at (s, idx).
+struct FusedArgs {
+    LeafArgs la;           // la.cnt / la.off = leaf_cnt / leaf_off
+    u64 N, seed;
+    int s, D, lb;
+    u64 idx, root_cnt;
+    u32 *leaf_cnt;
+    u64 *leaf_off;
+};
+#ifndef RS_FUSED_MAXD
+#define RS_FUSED_MAXD 11   // trees of <= 2^11 leaves (<= 128 CTAs: one wave)
+#endif
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wor_tu(FusedArgs f);
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wor_tu_p2(FusedArgs f);
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wr(FusedArgs f);
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wr_p2(FusedArgs f);
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wor(FusedArgs f);
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wr(FusedArgs f);
 // Ordered linear-probing leaf kernels (rs_leaf_lp.cuh): the default WOR / WR path.
 #ifndef RS_LP_WARPS
 #define RS_LP_WARPS 16

@@ -108,6 +108,8 @@ def test_set_option_host_only():
     rs.set_option(rs.OPT_LEAF_PATH, 0)
     rs.set_option(rs.OPT_TOPUP_MAX, 0)
     rs.set_option(rs.OPT_TOPUP_MAX, 32)
+    rs.set_option(rs.OPT_FUSED, 0)
+    rs.set_option(rs.OPT_FUSED, 1)
     with pytest.raises(rs.RSError):
         rs.set_option(rs.OPT_TOPUP_MAX, 33)
     with pytest.raises(rs.RSError):

@@ -106,6 +106,32 @@ def test_lp_path(N, n):
     _no_device_errors()
 
 
+# split + leaves in one launch (RS_OPT_FUSED, default on for shard trees of
+# <= 2^11 leaves on the warp-leaf paths; rs_fused.cuh) against the separate
+# split / leaf launches and the oracle: 32-bit power-of-two and Lemire leaves,
+# wide (> 2^32) leaves, depth < 4 (fewer leaves than one CTA's warps), the
+# largest fused depth (11) and the first unfused one (12), shards (s > 0)
+FUSED_CASES = [(2 ** 30, 2 ** 20), (2 ** 50, 2 ** 10), (2 ** 50, 2 ** 20), (10 ** 12 + 7, 123457),
+               (2 ** 40, 2 ** 21), (2 ** 40, 2 ** 22), (2 ** 45, 3000), (2 ** 20, 2 ** 14)]
+
+
+@pytest.mark.parametrize("N,n", FUSED_CASES)
+def test_fused_vs_separate(N, n):
+    for mode, f, orc in ((0, rs.sample_wor, O.sample_wor), (1, rs.sample_wr, O.sample_wr)):
+        fused = _np(f(N, n, 3))
+        shard = _np(rs.sample_wor_shard(N, n, 3, 4, 1) if mode == 0 else rs.sample_wr_shard(N, n, 3, 4, 1))
+        rs.set_option(rs.OPT_FUSED, 0)
+        try:
+            sep = _np(f(N, n, 3))
+            sep_shard = _np(rs.sample_wor_shard(N, n, 3, 4, 1) if mode == 0 else rs.sample_wr_shard(N, n, 3, 4, 1))
+        finally:
+            rs.set_option(rs.OPT_FUSED, 1)
+        assert np.array_equal(fused, sep), (N, n, mode)
+        assert np.array_equal(shard, sep_shard), (N, n, mode)
+        assert np.array_equal(fused, orc(N, n, 3)), (N, n, mode)
+    _no_device_errors()
+
+
 # ---- with replacement --------------------------------------------------------
 
 WR_CASES = [(1, 5), (4, 1000), (2, 3), (100, 100), (2 ** 24, 2 ** 20), (10 ** 9 + 7, 100003),
