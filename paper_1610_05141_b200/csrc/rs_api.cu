@@ -241,9 +241,12 @@ bool run_fused(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t st)
     la.spill_n = status + 1;
     la.spill = status + 4;
     f.N = p.N; f.seed = p.seed; f.s = p.s; f.D = p.D;
-    f.lb = depth < FUSED_LB ? depth : FUSED_LB;
+    f.lb = depth < FUSED_LB ? depth : depth > FUSED_LB + RS_FUSED_CTA_LOG ? depth - RS_FUSED_CTA_LOG : FUSED_LB;
+    la.span_log = (u32)f.lb;
     f.idx = p.idx; f.root_cnt = p.root_cnt;
     f.leaf_cnt = leaf_cnt; f.leaf_off = leaf_off;
+    f.lv_cnt[0] = (u64 *)(ws + p.o_ping_cnt); f.lv_off[0] = (u64 *)(ws + p.o_ping_off);
+    f.lv_cnt[1] = (u64 *)(ws + p.o_pong_cnt); f.lv_off[1] = (u64 *)(ws + p.o_pong_off);
     void (*fk)(FusedArgs) = wide ? (wr ? k_fused_wide_wr : k_fused_wide_wor)
                           : wr ? (p2 ? k_fused_wr_p2 : k_fused_wr)
                                : (p2 ? k_fused_wor_tu_p2 : k_fused_wor_tu);

@@ -180,6 +180,7 @@ struct LeafArgs {
     u32 *status;           // per-call status word (bit 0: a leaf exceeded the on-chip capacity)
     u32 cap;               // CTA kernel draw capacity (0: LEAF_CAP; rs_set_option(RS_OPT_LEAF_CAP), tests)
     u32 lp_cr;             // LP kernels: ceil_log2 of the launch's largest leaf range (generation tag shift)
+    u32 span_log;          // fused kernels: CTA c owns leaves [c << span_log, (c + 1) << span_log)
 };
 
 __global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_wor32(LeafArgs a);
@@ -214,15 +215,19 @@ __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wide_wr
 // Small trees: split + leaves in one launch (rs_fused.cuh); CTA c owns the
 // WL_WARPS leaves under node c at depth D - lb of the shard rooted at (s, idx).
 struct FusedArgs {
-    LeafArgs la;           // la.cnt / la.off = leaf_cnt / leaf_off
+    LeafArgs la;           // la.cnt / la.off = leaf_cnt / leaf_off, la.span_log = lb
     u64 N, seed;
     int s, D, lb;
     u64 idx, root_cnt;
     u32 *leaf_cnt;
     u64 *leaf_off;
+    u64 *lv_cnt[2], *lv_off[2];   // intermediate levels wider than a CTA's warps (ws ping / pong)
 };
 #ifndef RS_FUSED_MAXD
-#define RS_FUSED_MAXD 11   // trees of <= 2^11 leaves (<= 128 CTAs: one wave)
+#define RS_FUSED_MAXD 14   // shard trees of <= 2^14 leaves (deeper: the per-lane levels are slower than the level kernels)
+#endif
+#ifndef RS_FUSED_CTA_LOG
+#define RS_FUSED_CTA_LOG 7 // at most 2^7 CTAs (one wave of one 16-warp CTA per SM): deeper trees give each CTA more levels
 #endif
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wor_tu(FusedArgs f);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wor_tu_p2(FusedArgs f);

@@ -783,31 +783,32 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
     return 0;
 }
 
-template <bool WR, bool GR, bool TU, bool P2 = false>
-__device__ __forceinline__ void warp_leaves(const LeafArgs &a)
+template <bool WR, bool GR, bool TU, bool P2 = false, bool CS = false>
+__device__ __forceinline__ void warp_leaves(const LeafArgs &a)   // CS: CTA-span leaf ranges (fused kernels)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WarpLeaf &sh = reinterpret_cast<WarpLeaf *>(smem_raw)[wid];
     wl_clear(sh, lane);
     __syncwarp();
-    const u64 stride = (u64)gridDim.x * WL_WARPS;
-    u64 L = (u64)blockIdx.x * WL_WARPS + wid;
+    const u64 stride = CS ? (u64)WL_WARPS : (u64)gridDim.x * WL_WARPS;
+    u64 L = CS ? ((u64)blockIdx.x << a.span_log) + wid : (u64)blockIdx.x * WL_WARPS + wid;
+    const u64 Lend = CS ? min(a.nleaves, ((u64)blockIdx.x + 1) << a.span_log) : a.nleaves;
     // the next leaf's count / offset arrive by cp.async straight into shared
     // memory while this leaf is processed (no register stays live for them)
     const u32 s_k = (u32)__cvta_generic_to_shared(&sh.pf_k), s_off = (u32)__cvta_generic_to_shared(&sh.pf_off);
-    if (lane == 0 && L < a.nleaves) {
+    if (lane == 0 && L < Lend) {
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s_k), "l"(a.cnt + L) : "memory");
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s_off), "l"(a.off + L) : "memory");
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    for (; L < a.nleaves; L += stride) {
+    for (; L < Lend; L += stride) {
         if (lane == 0) asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
         const u32 k = sh.pf_k;
         const u64 off = sh.pf_off;
         __syncwarp();
-        if (lane == 0 && L + stride < a.nleaves) {   // prefetch the next leaf's count and offset
+        if (lane == 0 && L + stride < Lend) {   // prefetch the next leaf's count and offset
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s_k), "l"(a.cnt + L + stride) : "memory");
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s_off), "l"(a.off + L + stride) : "memory");
             asm volatile("cp.async.commit_group;" ::: "memory");

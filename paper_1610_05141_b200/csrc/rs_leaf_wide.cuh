@@ -165,29 +165,30 @@ __device__ __forceinline__ bool ww_finish(WarpLeafW &sh, u32 J, u32 h, u32 P, u6
     return true;
 }
 
-template <bool WR>
-__device__ __forceinline__ void warp_leaves_wide(const LeafArgs &a)
+template <bool WR, bool CS = false>
+__device__ __forceinline__ void warp_leaves_wide(const LeafArgs &a)   // CS: CTA-span leaf ranges (fused kernels)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WarpLeafW &sh = reinterpret_cast<WarpLeafW *>(smem_raw)[wid];
     wl_clear(sh.w, lane);
     __syncwarp();
-    const u64 stride = (u64)gridDim.x * WL_WARPS;
-    u64 L = (u64)blockIdx.x * WL_WARPS + wid;
+    const u64 stride = CS ? (u64)WL_WARPS : (u64)gridDim.x * WL_WARPS;
+    u64 L = CS ? ((u64)blockIdx.x << a.span_log) + wid : (u64)blockIdx.x * WL_WARPS + wid;
+    const u64 Lend = CS ? min(a.nleaves, ((u64)blockIdx.x + 1) << a.span_log) : a.nleaves;
     const u32 s_k = (u32)__cvta_generic_to_shared(&sh.w.pf_k), s_off = (u32)__cvta_generic_to_shared(&sh.w.pf_off);
-    if (lane == 0 && L < a.nleaves) {
+    if (lane == 0 && L < Lend) {
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s_k), "l"(a.cnt + L) : "memory");
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s_off), "l"(a.off + L) : "memory");
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    for (; L < a.nleaves; L += stride) {
+    for (; L < Lend; L += stride) {
         if (lane == 0) asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
         const u32 k = sh.w.pf_k;
         const u64 off = sh.w.pf_off;
         __syncwarp();
-        if (lane == 0 && L + stride < a.nleaves) {
+        if (lane == 0 && L + stride < Lend) {
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s_k), "l"(a.cnt + L + stride) : "memory");
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s_off), "l"(a.off + L + stride) : "memory");
             asm volatile("cp.async.commit_group;" ::: "memory");
