@@ -6,6 +6,15 @@
 
 namespace rs {
 
+// Checked builds (-DRS_CHECKED, tools/checked_suite.sh): shared-memory index
+// checks in the leaf kernels' scatter; a violation sets bit 8 of the sticky
+// device error word (rs_device_errors), which every parity test asserts is 0.
+#ifdef RS_CHECKED
+#define RS_CHK(c) do { if (!(c)) atomicOr(&g_rs_errors, 0x100u); } while (0)
+#else
+#define RS_CHK(c) do { } while (0)
+#endif
+
 // Sticky device error flags (rs_device_errors): bit 0 leaf capacity,
 // bit 1 Bernoulli chunk capacity.  Defined in rs_kernels.cu (librs.cu is a
 // single translation unit).

@@ -384,7 +384,7 @@ __device__ __forceinline__ void wl_scatter_reg(WarpLeaf &sh, u32 J, u32 h, u32 M
             // atomics first, stores after (smem stores and atomics may alias as far
             // as the compiler knows: interleaving would serialise every round trip)
 #pragma unroll
-            for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) kh[pos[e - 4 * m0]] = x[e];
+            for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) { RS_CHK(h + pos[e - 4 * m0] < (u32)WL_CAP); kh[pos[e - 4 * m0]] = x[e]; }
         } else if (128u * m0 < J) {
 #pragma unroll
             for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) {
@@ -393,7 +393,7 @@ __device__ __forceinline__ void wl_scatter_reg(WarpLeaf &sh, u32 J, u32 h, u32 M
             }
 #pragma unroll
             for (int e = 4 * m0; e < 4 * (m0 + GB); ++e)
-                if (pos[e - 4 * m0] != (u32)WL_CAP) kh[pos[e - 4 * m0]] = x[e];
+                if (pos[e - 4 * m0] != (u32)WL_CAP) { RS_CHK(h + pos[e - 4 * m0] < (u32)WL_CAP); kh[pos[e - 4 * m0]] = x[e]; }
         }
     }
     __syncwarp();
@@ -488,7 +488,7 @@ __device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const RoundKeys &K, con
                 pos[e - 4 * m0] = WL_POS(e);
 #endif
 #pragma unroll
-            for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) kh[pos[e - 4 * m0]] = x[e];
+            for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) { RS_CHK(h + pos[e - 4 * m0] < (u32)WL_CAP); kh[pos[e - 4 * m0]] = x[e]; }
         } else if (4 * (lane + 32u * m0) < J) {
 #pragma unroll
             for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) {
@@ -497,7 +497,7 @@ __device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const RoundKeys &K, con
             }
 #pragma unroll
             for (int e = 4 * m0; e < 4 * (m0 + GB); ++e)
-                if (pos[e - 4 * m0] != (u32)WL_CAP) kh[pos[e - 4 * m0]] = x[e];
+                if (pos[e - 4 * m0] != (u32)WL_CAP) { RS_CHK(h + pos[e - 4 * m0] < (u32)WL_CAP); kh[pos[e - 4 * m0]] = x[e]; }
         }
     }
 #undef WL_POS

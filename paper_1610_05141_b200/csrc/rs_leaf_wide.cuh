@@ -90,7 +90,7 @@ __device__ __forceinline__ void ww_scatter(WarpLeafW &sh, u32 J, u32 h, u32 lane
         }
 #pragma unroll
         for (int t = 0; t < 4; ++t)
-            if (pos[t] != (u32)WL_CAP) { kh[pos[t]] = x[4 * m + t]; lh[pos[t]] = l[4 * m + t]; }
+            if (pos[t] != (u32)WL_CAP) { RS_CHK(h + pos[t] < (u32)WL_CAP); kh[pos[t]] = x[4 * m + t]; lh[pos[t]] = l[4 * m + t]; }
     }
     __syncwarp();
 }
