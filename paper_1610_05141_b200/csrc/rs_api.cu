@@ -742,14 +742,14 @@ __global__ void k_deviates(int kind, u64 k, u64 L, u64 R, u64 seed, u64 id0, u64
         out[i] = kind ? binom(k, L, R, seed, id0 + i) : hgd(k, L, R, seed, id0 + i);
 }
 
-// The lane-group deviates (hgd_grp / binom_grp): G lanes per deviate.
+// The lane-group deviates (hgd_tpg / binom_grp): G lanes per deviate.
 template <int G>
 __global__ void k_deviates_grp(int kind, u64 k, u64 L, u64 R, u64 seed, u64 id0, u64 count, u64 *out)
 {
     const u64 ngrp = (u64)gridDim.x * blockDim.x / G;
     for (u64 i = (blockIdx.x * (u64)blockDim.x + threadIdx.x) / G; i < count; i += ngrp) {
         const u64 x = G == 32 ? (kind ? binom_tp(k, L, R, seed, id0 + i) : hgd_tp(k, L, R, seed, id0 + i))
-                              : (kind ? binom_grp<G>(k, L, R, seed, id0 + i) : hgd_grp<G>(k, L, R, seed, id0 + i));
+                              : (kind ? binom_grp<G>(k, L, R, seed, id0 + i) : hgd_tpg<G>(k, L, R, seed, id0 + i));
         if ((threadIdx.x & (G - 1)) == 0) out[i] = x;
     }
 }

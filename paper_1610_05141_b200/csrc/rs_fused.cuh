@@ -87,7 +87,7 @@ __device__ __forceinline__ void fused_split(const FusedArgs &f)
     int cur = 0;
     for (int l = 0; l < lb; ++l) {
         const u32 width = 1u << l;
-        // a warp per node (hgd_tp), or 8 lanes per node (hgd_grp<8>); wider
+        // a warp per node (hgd_tp), or 8 lanes per node (hgd_tpg<8>); wider
         // levels (a lane per node) measured slower than the level kernels
         if (width <= (u32)WL_WARPS) {
             if (wid < width) fused_node<WR, 32>(f, fs_cnt, fs_off, l, cur, wid, dp, c);

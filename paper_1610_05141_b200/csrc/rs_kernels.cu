@@ -48,7 +48,7 @@ __device__ __forceinline__ void split_top(const SplitArgs &a)
         const int d = a.ds + l;
         const u64 base = node << l;
         // narrow levels: a group of G lanes per node evaluates G rejection
-        // iterations at once (hgd_grp), so a level costs ~one iteration's latency
+        // iterations at once (hgd_tpg), so a level costs ~one iteration's latency
         // (a warp per node -- hgd_tp -- up to four nodes per warp)
         if (width * 32 <= 4 * SPLIT_NT) split_top_level<WR, 32>(a, buf[cur], buf[cur ^ 1], width, d, base);
         else if (width * 8 <= SPLIT_NT) split_top_level<WR, 8>(a, buf[cur], buf[cur ^ 1], width, d, base);
