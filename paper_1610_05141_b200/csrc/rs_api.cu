@@ -469,9 +469,9 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         la.spill_n = spill_n;
         la.spill = status + 4;
         void (*wk)(LeafArgs) = wr ? k_leaf_warp_wide_wr : k_leaf_warp_wide_wor;
-        const size_t wsm = sizeof(WarpLeafW) * WL_WARPS;
-        const unsigned g1 = leaf_grid((const void *)wk, 32 * WL_WARPS, wsm, (p.nleaves + WL_WARPS - 1) / WL_WARPS);
-        wk<<<g1, 32 * WL_WARPS, wsm, st>>>(la);
+        const size_t wsm = sizeof(WarpLeafW) * WW_WARPS;
+        const unsigned g1 = leaf_grid((const void *)wk, 32 * WW_WARPS, wsm, (p.nleaves + WW_WARPS - 1) / WW_WARPS);
+        wk<<<g1, 32 * WW_WARPS, wsm, st>>>(la);
         ++t_launches;
         LeafArgs lb = la;
         lb.spill = nullptr; lb.spill_n = nullptr;

@@ -219,8 +219,15 @@ __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu_
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr_p2(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_p2(LeafArgs a);
 // wide leaf ranges (> 2^32 - 4096): 31-bit keys + payload (rs_leaf_wide.cuh)
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wide_wor(LeafArgs a);
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wide_wr(LeafArgs a);
+#ifndef RS_WW_WARPS
+#define RS_WW_WARPS 12      // 167 registers (16 warps: 128 with 384 B spills; measured n = 2^28 leaf sweep 2.28 -> 1.90 ms)
+#endif
+#ifndef RS_WW_MINB
+#define RS_WW_MINB 1
+#endif
+constexpr int WW_WARPS = RS_WW_WARPS;   // warps per CTA of the wide kernels
+__global__ void __launch_bounds__(32 * WW_WARPS, RS_WW_MINB) k_leaf_warp_wide_wor(LeafArgs a);
+__global__ void __launch_bounds__(32 * WW_WARPS, RS_WW_MINB) k_leaf_warp_wide_wr(LeafArgs a);
 // Small trees: split + leaves in one launch (rs_fused.cuh); CTA c owns the
 // WL_WARPS leaves under node c at depth D - lb of the shard rooted at (s, idx).
 struct FusedArgs {

@@ -165,7 +165,7 @@ __device__ __forceinline__ bool ww_finish(WarpLeafW &sh, u32 J, u32 h, u32 P, u6
     return true;
 }
 
-template <bool WR, bool CS = false>
+template <bool WR, bool CS = false, int NW = WL_WARPS>
 __device__ __forceinline__ void warp_leaves_wide(const LeafArgs &a)   // CS: CTA-span leaf ranges (fused kernels)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -173,8 +173,8 @@ __device__ __forceinline__ void warp_leaves_wide(const LeafArgs &a)   // CS: CTA
     WarpLeafW &sh = reinterpret_cast<WarpLeafW *>(smem_raw)[wid];
     wl_clear(sh.w, lane);
     __syncwarp();
-    const u64 stride = CS ? (u64)WL_WARPS : (u64)gridDim.x * WL_WARPS;
-    u64 L = CS ? ((u64)blockIdx.x << a.span_log) + wid : (u64)blockIdx.x * WL_WARPS + wid;
+    const u64 stride = CS ? (u64)NW : (u64)gridDim.x * NW;
+    u64 L = CS ? ((u64)blockIdx.x << a.span_log) + wid : (u64)blockIdx.x * NW + wid;
     const u64 Lend = CS ? min(a.nleaves, ((u64)blockIdx.x + 1) << a.span_log) : a.nleaves;
     const u32 s_k = (u32)__cvta_generic_to_shared(&sh.w.pf_k), s_off = (u32)__cvta_generic_to_shared(&sh.w.pf_off);
     if (lane == 0 && L < Lend) {
@@ -217,7 +217,7 @@ __device__ __forceinline__ void warp_leaves_wide(const LeafArgs &a)   // CS: CTA
     }
 }
 
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wide_wor(LeafArgs a) { warp_leaves_wide<false>(a); }
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wide_wr(LeafArgs a) { warp_leaves_wide<true>(a); }
+__global__ void __launch_bounds__(32 * WW_WARPS, RS_WW_MINB) k_leaf_warp_wide_wor(LeafArgs a) { warp_leaves_wide<false, false, WW_WARPS>(a); }
+__global__ void __launch_bounds__(32 * WW_WARPS, RS_WW_MINB) k_leaf_warp_wide_wr(LeafArgs a) { warp_leaves_wide<true, false, WW_WARPS>(a); }
 
 }  // namespace rs

@@ -15,7 +15,7 @@ import paper_1610_05141_b200 as rs  # noqa: E402
 N = 2 ** 50
 print(f"# rs_sample_wor, N = 2^50, one B200, CUDA events ({torch.cuda.get_device_name()})")
 print(f"# {'n':>8} {'reps':>6} {'us/call':>10} {'ns/sample':>10} {'samples/s':>10}  D  {'graph us/call':>13} {'graph samples/s':>15}")
-for e in range(10, 33, 2):
+for e in ([int(x) for x in sys.argv[1:]] or range(10, 33, 2)):
     n = 2 ** e
     out = torch.empty(n, dtype=torch.uint64, device="cuda")
     ws = torch.empty(rs.workspace_bytes(rs.MODE_WOR, N, n), dtype=torch.uint8, device="cuda")
