@@ -446,10 +446,11 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
                                                ? (p2 ? (!tu && RS_WL_P2_PLAIN ? k_leaf_warp_wor_p2 : k_leaf_warp_wor_tu_p2)
                                                      : k_leaf_warp_wor_tu)
                                                : k_leaf_warp_wor);
-            const size_t wsm = sizeof(WarpLeaf) * WL_WARPS;
-            const u64 wgrid = (p.nleaves + WL_WARPS - 1) / WL_WARPS;
-            const unsigned g1 = leaf_grid((const void *)wk, 32 * WL_WARPS, wsm, wgrid);
-            wk<<<g1, 32 * WL_WARPS, wsm, st>>>(la);
+            const int nw = (wr && p2) ? WR_WARPS : WL_WARPS;
+            const size_t wsm = sizeof(WarpLeaf) * nw;
+            const u64 wgrid = (p.nleaves + nw - 1) / nw;
+            const unsigned g1 = leaf_grid((const void *)wk, 32 * nw, wsm, wgrid);
+            wk<<<g1, 32 * nw, wsm, st>>>(la);
         }
         ++t_launches;
         LeafArgs lb = la;

@@ -216,7 +216,11 @@ __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm(Lea
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm_tu(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu_p2(LeafArgs a);
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr_p2(LeafArgs a);
+#ifndef RS_WR_WARPS
+#define RS_WR_WARPS 16
+#endif
+constexpr int WR_WARPS = RS_WR_WARPS;   // warps per CTA of the power-of-two WR kernel
+__global__ void __launch_bounds__(32 * WR_WARPS, RS_WL_MINB) k_leaf_warp_wr_p2(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_p2(LeafArgs a);
 // wide leaf ranges (> 2^32 - 4096): 31-bit keys + payload (rs_leaf_wide.cuh)
 #ifndef RS_WW_WARPS

@@ -300,6 +300,9 @@ __device__ __forceinline__ u32 wl_scan(WarpLeaf &sh, u32 lane)
 #ifndef RS_WL_REG
 #define RS_WL_REG 0         // 1: draws stay in registers from the count to the scatter (no staging round trip) in every kernel
 #endif
+#ifndef RS_WL_REG_WR
+#define RS_WL_REG_WR 0      // register-resident count/scatter in the power-of-two WR kernel
+#endif
 #ifndef RS_WL_REG_P2
 #define RS_WL_REG_P2 1      // ... in the power-of-two WOR kernels only (spill-free there)
 #endif
@@ -783,7 +786,7 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
     return 0;
 }
 
-template <bool WR, bool GR, bool TU, bool P2 = false, bool CS = false>
+template <bool WR, bool GR, bool TU, bool P2 = false, bool CS = false, int NW = WL_WARPS>
 __device__ __forceinline__ void warp_leaves(const LeafArgs &a)   // CS: CTA-span leaf ranges (fused kernels)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -791,8 +794,8 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)   // CS: CTA-span
     WarpLeaf &sh = reinterpret_cast<WarpLeaf *>(smem_raw)[wid];
     wl_clear(sh, lane);
     __syncwarp();
-    const u64 stride = CS ? (u64)WL_WARPS : (u64)gridDim.x * WL_WARPS;
-    u64 L = CS ? ((u64)blockIdx.x << a.span_log) + wid : (u64)blockIdx.x * WL_WARPS + wid;
+    const u64 stride = CS ? (u64)NW : (u64)gridDim.x * NW;
+    u64 L = CS ? ((u64)blockIdx.x << a.span_log) + wid : (u64)blockIdx.x * NW + wid;
     const u64 Lend = CS ? min(a.nleaves, ((u64)blockIdx.x + 1) << a.span_log) : a.nleaves;
     // the next leaf's count / offset arrive by cp.async straight into shared
     // memory while this leaf is processed (no register stays live for them)
@@ -832,7 +835,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)   // CS: CTA-span
         // the register-resident count/scatter: for the power-of-two WOR kernels
         // (no spills there; measured headline 12.45 -> 12.26 ms, cfg1 4.64 ->
         // 4.33) or everywhere with RS_WL_REG (spills elsewhere; WR slower)
-        constexpr bool REG = RS_WL_REG || (RS_WL_REG_P2 && P2 && !WR && !GR);
+        constexpr bool REG = RS_WL_REG || (RS_WL_REG_P2 && P2 && !WR && !GR) || (RS_WL_REG_WR && P2 && WR && !GR);
         const u32 M = REG ? wl_bucket_mult(cr) : 0u;
         for (;;) {
             u32 res = 0xffffffffu;
@@ -898,7 +901,7 @@ __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm(Lea
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm_tu(LeafArgs a) { warp_leaves<false, true, true>(a); }
 // every leaf range a power of two (N = 2^a): no Lemire rejection code at all
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu_p2(LeafArgs a) { warp_leaves<false, false, true, true>(a); }
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr_p2(LeafArgs a) { warp_leaves<true, false, false, true>(a); }
+__global__ void __launch_bounds__(32 * WR_WARPS, RS_WL_MINB) k_leaf_warp_wr_p2(LeafArgs a) { warp_leaves<true, false, false, true, false, WR_WARPS>(a); }
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_p2(LeafArgs a) { warp_leaves<false, false, false, true>(a); }
 
 }  // namespace rs
