@@ -409,6 +409,11 @@ def run_native(args):
                 kname += "_tu"
             if mode in ("wor", "wr") and (N & (N - 1)) == 0:     # power-of-two N: the _p2 kernels
                 kname += "_p2"
+        # shard trees of depth <= 14 on the warp paths: split + leaves in one
+        # launch (rs_fused.cuh); its time is the "leaf" class, split_ms ~ 0
+        if mode in ("wor", "wr") and not comp and kname.startswith("k_leaf_warp_") and \
+                D - (world - 1).bit_length() <= 14:
+            kname = kname.replace("k_leaf_warp_", "k_fused_")
     kms_per = kms / max(kl, 1)
     achieved = bytes_per_launch / (kms_per / 1e3) / 1e9 if kms_per > 0 else None
     traffic, winst = None, None

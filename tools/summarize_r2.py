@@ -92,7 +92,9 @@ def main():
             open(os.path.join(OD, f"full_{tag}_hotlines.txt"), "w").write(hot)
     json.dump(traffic, open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
     for name, out in (("r2_sweep.txt", "sweep.txt"), ("r2_ubench.txt", "ubench.txt"),
-                      ("r2_hgd_lat.txt", "hgd_lat.txt"), ("r2_box.txt", "box.txt"), ("r2_smoke.log", "smoke.txt")):
+                      ("r2_hgd_lat.txt", "hgd_lat.txt"), ("r2_box.txt", "box.txt"), ("r2_smoke.log", "smoke.txt"),
+                      ("r2_checked.txt", "checked_suite.txt"), ("guards.log", "guards_tail.txt"),
+                      ("checked.log", "checked_tail.txt")):
         p = os.path.join(G, name)
         if os.path.exists(p):
             shutil.copy(p, os.path.join(OD, out))
