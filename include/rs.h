@@ -272,10 +272,14 @@ rs_status rs_device_errors(int clear, unsigned *flags);
  * D - s <= 11) on the warp-leaf paths run split and leaves in one launch,
  * each CTA walking the path from the shard root to its 16-leaf subtree
  * (n up to ~2^21; rs_fused.cuh); 0 = the separate split and leaf launches.
+ * RS_OPT_WARP_CAP: 0 (default) or 1..1152: the warp-per-leaf kernels hand
+ * every leaf of more draws to the CTA kernel's spill pass (tests: covers
+ * that path, normally taken by ~1 leaf in 10^4).
  * Results are identical for every setting of LEAF_PATH, TOPUP_MAX,
- * SPLIT_COOP and FUSED (LEAF_CAP changes which leaves fail).  Unknown option
+ * SPLIT_COOP, FUSED and WARP_CAP (LEAF_CAP changes which leaves fail).  Unknown option
  * or value -> RS_EINVAL. */
-enum { RS_OPT_LEAF_PATH = 1, RS_OPT_TOPUP_MAX = 2, RS_OPT_LEAF_CAP = 3, RS_OPT_SPLIT_COOP = 4, RS_OPT_FUSED = 5 };
+enum { RS_OPT_LEAF_PATH = 1, RS_OPT_TOPUP_MAX = 2, RS_OPT_LEAF_CAP = 3, RS_OPT_SPLIT_COOP = 4, RS_OPT_FUSED = 5,
+       RS_OPT_WARP_CAP = 6 };
 rs_status rs_set_option(int option, int value);
 
 /* Number of kernel launches issued by this thread since the last reset. */

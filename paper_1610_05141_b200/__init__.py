@@ -346,6 +346,7 @@ OPT_TOPUP_MAX = 2
 OPT_LEAF_CAP = 3
 OPT_SPLIT_COOP = 4
 OPT_FUSED = 5
+OPT_WARP_CAP = 6
 
 
 def node_info(mode: int, N: int, n: int, seed: int, depth: int, index: int):

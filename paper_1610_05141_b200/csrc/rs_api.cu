@@ -22,6 +22,7 @@ int g_topup_max = 32;                   // rs_set_option(RS_OPT_TOPUP_MAX)
 int g_leaf_cap = 0;                     // rs_set_option(RS_OPT_LEAF_CAP) (tests: force overflows)
 int g_split_coop = 1;                   // rs_set_option(RS_OPT_SPLIT_COOP): cooperative top of the split tree
 int g_fused = 1;                        // rs_set_option(RS_OPT_FUSED): small trees in one launch (rs_fused.cuh)
+int g_warp_cap = 0;                     // rs_set_option(RS_OPT_WARP_CAP): warp kernels spill leaves above it (tests)
 #ifndef RS_WL_WOR_TU_ALL
 #define RS_WL_WOR_TU_ALL 1
 #endif
@@ -237,6 +238,7 @@ bool run_fused(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t st)
     la.rk = round_keys(p.seed);
     la.status = status;
     la.cap = (u32)g_leaf_cap;
+    la.wcap = (u32)g_warp_cap;
     la.topup_max = (u32)g_topup_max;
     la.spill_n = status + 1;
     la.spill = status + 4;
@@ -247,22 +249,27 @@ bool run_fused(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t st)
     f.leaf_cnt = leaf_cnt; f.leaf_off = leaf_off;
     f.lv_cnt[0] = (u64 *)(ws + p.o_ping_cnt); f.lv_off[0] = (u64 *)(ws + p.o_ping_off);
     f.lv_cnt[1] = (u64 *)(ws + p.o_pong_cnt); f.lv_off[1] = (u64 *)(ws + p.o_pong_off);
-    void (*fk)(FusedArgs) = wide ? (wr ? k_fused_wide_wr : k_fused_wide_wor)
+    const bool wide_sep = wide && f.lb > FUSED_LB;            // wide, > 1 leaf per warp: spills launched apart
+    void (*fk)(FusedArgs) = wide ? (wide_sep ? (wr ? k_fused_wide_wr : k_fused_wide_wor)
+                                             : (wr ? k_fused_wide_wr_s : k_fused_wide_wor_s))
                           : wr ? (p2 ? k_fused_wr_p2 : k_fused_wr)
                                : (p2 ? k_fused_wor_tu_p2 : k_fused_wor_tu);
     const size_t fsm = wide ? sizeof(WarpLeafW) * WL_WARPS : sizeof(WarpLeaf) * WL_WARPS;
     (void)leaf_grid((const void *)fk, 32 * WL_WARPS, fsm, 1);      // (attributes)
     Span sp(1, st);
-    fk<<<1u << (depth - f.lb), 32 * WL_WARPS, fsm, st>>>(f);
+    static_assert(sizeof(SLeaf<u32>) <= sizeof(WarpLeaf) * WL_WARPS, "fused kernels: spills reuse the warps' smem");
+    fk<<<1u << (depth - f.lb), 32 * WL_WARPS, fsm, st>>>(f);   // (spilled leaves: its last CTA, unless wide_sep)
     ++t_launches;
-    LeafArgs lb = la;
-    lb.spill = nullptr; lb.spill_n = nullptr;
-    lb.list = status + 4; lb.list_n = status + 1;
-    void (*kern)(LeafArgs) = wide ? (wr ? k_leaf_wr64 : k_leaf_wor64) : (wr ? k_leaf_wr32 : k_leaf_wor32);
-    const size_t sm = wide ? sizeof(SLeaf<u64>) : sizeof(SLeaf<u32>);
-    const unsigned g2 = leaf_grid((const void *)kern, LEAF_NT, sm, p.nleaves < 2ull * 148 ? p.nleaves : 2ull * 148);
-    kern<<<g2, LEAF_NT, sm, st>>>(lb);
-    ++t_launches;
+    if (wide_sep) {                                             // the CTA kernel with u64 keys
+        LeafArgs lb = la;
+        lb.spill = nullptr; lb.spill_n = nullptr;
+        lb.list = status + 4; lb.list_n = status + 1;
+        void (*kern)(LeafArgs) = wr ? k_leaf_wr64 : k_leaf_wor64;
+        const unsigned g2 = leaf_grid((const void *)kern, LEAF_NT, sizeof(SLeaf<u64>),
+                                      p.nleaves < 2ull * 148 ? p.nleaves : 2ull * 148);
+        kern<<<g2, LEAF_NT, sizeof(SLeaf<u64>), st>>>(lb);
+        ++t_launches;
+    }
     sp.end();
     return true;
 }
@@ -389,6 +396,7 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
     la.gV = p.gV;
     la.status = status;
     la.cap = (u32)g_leaf_cap;
+    la.wcap = (u32)g_warp_cap;
     const bool wide = p.r_max > 0xfffff000ull;    // u32 keys (below the warp kernel's sentinels)
     const bool wr = (p.mode == RS_MODE_WR);
     void (*kern)(LeafArgs);
@@ -1198,6 +1206,10 @@ rs_status rs_set_option(int option, int value)
     }
     if (option == RS_OPT_FUSED && (value == 0 || value == 1)) {
         g_fused = value;
+        return ret(RS_OK);
+    }
+    if (option == RS_OPT_WARP_CAP && value >= 0 && value <= WL_CAP) {
+        g_warp_cap = value;
         return ret(RS_OK);
     }
     if (option == RS_OPT_LEAF_CAP && value >= 0 && value <= LEAF_CAP) {

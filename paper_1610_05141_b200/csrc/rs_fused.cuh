@@ -15,7 +15,8 @@
 // by every CTA: the chain is the same D - s deviates either way, and no CTA
 // waits for another.  Every count is the tree's (same deviate keyed by the
 // same node id), so the output is bit-identical to the split kernels'.  Then
-// the CTA's warps run the warp-per-leaf kernel body over its own leaves.
+// the CTA's warps run the warp-per-leaf kernel body over its own leaves, and
+// the last CTA completes the (rare) spilled leaves.
 #pragma once
 
 namespace rs {
@@ -99,17 +100,44 @@ __device__ __forceinline__ void fused_split(const FusedArgs &f)
     }
 }
 
+// The leaves the warp bodies spilled (usually none): the LAST CTA to finish
+// its leaves (a counter in the call's status header, zeroed with it) runs
+// them through the CTA-per-leaf routine, in the shared memory the warps no
+// longer use -- instead of a second launch.
+static_assert(LEAF_NT == 32 * WL_WARPS, "fused kernels: the CTA leaf routine's thread count");
+template <typename K, bool WR>
+__device__ __forceinline__ void fused_spills(const LeafArgs &a)
+{
+    __shared__ u32 last;
+    __threadfence();                                      // every warp's spill-list entries ...
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        last = atomicAdd(a.status + 3, 1u) == gridDim.x - 1;   // ... before this CTA's arrival
+        if (last) __threadfence();
+    }
+    __syncthreads();
+    if (last) sample_leaves<K, WR, true>(a);
+}
+
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wor_tu(FusedArgs f)
-{ fused_split<false>(f); warp_leaves<false, false, true, false, true>(f.la); }
+{ fused_split<false>(f); warp_leaves<false, false, true, false, true>(f.la); fused_spills<u32, false>(f.la); }
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wor_tu_p2(FusedArgs f)
-{ fused_split<false>(f); warp_leaves<false, false, true, true, true>(f.la); }
+{ fused_split<false>(f); warp_leaves<false, false, true, true, true>(f.la); fused_spills<u32, false>(f.la); }
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wr(FusedArgs f)
-{ fused_split<true>(f); warp_leaves<true, false, false, false, true>(f.la); }
+{ fused_split<true>(f); warp_leaves<true, false, false, false, true>(f.la); fused_spills<u32, true>(f.la); }
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wr_p2(FusedArgs f)
-{ fused_split<true>(f); warp_leaves<true, false, false, true, true>(f.la); }
+{ fused_split<true>(f); warp_leaves<true, false, false, true, true>(f.la); fused_spills<u32, true>(f.la); }
+// Wide leaves: with the spills in the kernel (one leaf per warp: the saved
+// launch matters) or left to a separate CTA launch (more leaves per warp: the
+// u64 spill routine inlined costs the leaf body registers, n = 2^24 229 ->
+// 245 us; the host picks)
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wor(FusedArgs f)
 { fused_split<false>(f); warp_leaves_wide<false, true>(f.la); }
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wr(FusedArgs f)
 { fused_split<true>(f); warp_leaves_wide<true, true>(f.la); }
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wor_s(FusedArgs f)
+{ fused_split<false>(f); warp_leaves_wide<false, true>(f.la); fused_spills<u64, false>(f.la); }
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wr_s(FusedArgs f)
+{ fused_split<true>(f); warp_leaves_wide<true, true>(f.la); fused_spills<u64, true>(f.la); }
 
 }  // namespace rs

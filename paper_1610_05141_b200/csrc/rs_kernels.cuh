@@ -190,6 +190,7 @@ struct LeafArgs {
     u32 cap;               // CTA kernel draw capacity (0: LEAF_CAP; rs_set_option(RS_OPT_LEAF_CAP), tests)
     u32 lp_cr;             // LP kernels: ceil_log2 of the launch's largest leaf range (generation tag shift)
     u32 span_log;          // fused kernels: CTA c owns leaves [c << span_log, (c + 1) << span_log)
+    u32 wcap;              // warp kernels: != 0 spills every leaf of more draws (RS_OPT_WARP_CAP, tests)
 };
 
 __global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_wor32(LeafArgs a);
@@ -255,6 +256,8 @@ __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wr(FusedArg
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wr_p2(FusedArgs f);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wor(FusedArgs f);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wr(FusedArgs f);
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wor_s(FusedArgs f);
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wr_s(FusedArgs f);
 // Ordered linear-probing leaf kernels (rs_leaf_lp.cuh): the default WOR / WR path.
 #ifndef RS_LP_WARPS
 #define RS_LP_WARPS 16

@@ -416,15 +416,19 @@ __device__ __forceinline__ void leaf_init(SLeaf<K> &sh)
 }
 
 // WOR (a5/a6) and WR (a8) leaves: one CTA per leaf, grid-stride over leaves.
-template <typename K, bool WR>
+// SPILLS: only the leaves of a warp kernel's spill list (a.spill, *a.spill_n),
+// by one CTA (the fused kernels' last CTA).
+template <typename K, bool WR, bool SPILLS = false>
 __device__ __forceinline__ void sample_leaves(const LeafArgs &a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SLeaf<K> &sh = *reinterpret_cast<SLeaf<K> *>(smem_raw);
     leaf_init(sh);
-    const u64 nwork = a.list ? (u64)*a.list_n : a.nleaves;
-    for (u64 it = blockIdx.x; it < nwork; it += gridDim.x) {
-        const u64 L = a.list ? (u64)a.list[it] : it;
+    const u32 *list = SPILLS ? a.spill : a.list;
+    const u64 nwork = SPILLS ? (u64)*(volatile const u32 *)a.spill_n : list ? (u64)*a.list_n : a.nleaves;
+    const u64 first = SPILLS ? 0 : blockIdx.x, step = SPILLS ? 1 : gridDim.x;
+    for (u64 it = first; it < nwork; it += step) {
+        const u64 L = list ? (u64)((volatile const u32 *)list)[it] : it;
         const u32 k = a.cnt[L];
         if (k == 0) continue;
         const LeafGeom g = leaf_geom(a, L);

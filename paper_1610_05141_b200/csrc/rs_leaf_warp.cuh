@@ -817,6 +817,10 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)   // CS: CTA-span
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
         if (k == 0) continue;
+        if (a.wcap != 0u && k > a.wcap) {               // (tests: force the spill path)
+            if (lane == 0) a.spill[atomicAdd(a.spill_n, 1u)] = (u32)L;
+            continue;
+        }
         const LeafGeom g = leaf_geom(a, L);
         const int cr = ceil_log2(g.r);
         const WDrawer dr(Stream(a.seed, WR ? P_WR : P_WOR, g.id), g.r, cr);

@@ -194,6 +194,10 @@ __device__ __forceinline__ void warp_leaves_wide(const LeafArgs &a)   // CS: CTA
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
         if (k == 0) continue;
+        if (a.wcap != 0u && k > a.wcap) {               // (tests: force the spill path)
+            if (lane == 0) a.spill[atomicAdd(a.spill_n, 1u)] = (u32)L;
+            continue;
+        }
         const LeafGeom g = leaf_geom(a, L);
         const int cr = ceil_log2(g.r);                      // 32 .. 63
         const u32 shk = (u32)cr - (u32)WW_KEYBITS;          // key = x >> shk < 2^31

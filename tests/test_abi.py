@@ -110,6 +110,10 @@ def test_set_option_host_only():
     rs.set_option(rs.OPT_TOPUP_MAX, 32)
     rs.set_option(rs.OPT_FUSED, 0)
     rs.set_option(rs.OPT_FUSED, 1)
+    rs.set_option(rs.OPT_WARP_CAP, 900)
+    rs.set_option(rs.OPT_WARP_CAP, 0)
+    with pytest.raises(rs.RSError):
+        rs.set_option(rs.OPT_WARP_CAP, 5000)
     with pytest.raises(rs.RSError):
         rs.set_option(rs.OPT_TOPUP_MAX, 33)
     with pytest.raises(rs.RSError):

@@ -132,6 +132,27 @@ def test_fused_vs_separate(N, n):
     _no_device_errors()
 
 
+# the warp kernels' spill pass (normally ~1 leaf in 10^4: a leaf of > 1149
+# draws or a pathological bucket): RS_OPT_WARP_CAP hands most leaves to it --
+# the fused kernels' last CTA, or the separate CTA launch -- 32-bit and wide
+SPILL_CASES = [(2 ** 30, 2 ** 20), (2 ** 40, 2 ** 24), (2 ** 50, 2 ** 12), (2 ** 50, 2 ** 24), (10 ** 12 + 7, 123457)]
+
+
+@pytest.mark.parametrize("N,n", SPILL_CASES)
+def test_warp_spill_path(N, n):
+    rs.set_option(rs.OPT_WARP_CAP, 1000)
+    try:
+        got = _np(rs.sample_wor(N, n, 8))
+        gwr = _np(rs.sample_wr(N, n, 8))
+        gsh = _np(rs.sample_wor_shard(N, n, 8, 4, 2))
+    finally:
+        rs.set_option(rs.OPT_WARP_CAP, 0)
+    assert np.array_equal(got, O.sample_wor(N, n, 8))
+    assert np.array_equal(gwr, O.sample_wr(N, n, 8))
+    assert np.array_equal(gsh, _np(rs.sample_wor_shard(N, n, 8, 4, 2)))
+    _no_device_errors()
+
+
 # ---- with replacement --------------------------------------------------------
 
 WR_CASES = [(1, 5), (4, 1000), (2, 3), (100, 100), (2 ** 24, 2 ** 20), (10 ** 9 + 7, 100003),
