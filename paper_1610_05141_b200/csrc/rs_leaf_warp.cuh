@@ -697,19 +697,16 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
 #pragma unroll
             for (int i = 0; i < E; ++i) {
                 const u32 p = p0 + i;
-                nd += p > h && p < h + J && y[i] == (i ? y[i - 1] : prv);
+                nd += p > h && y[i] == (i ? y[i - 1] : prv);   // (sentinels: distinct, above every key)
             }
             const u32 ndup = __reduce_add_sync(0xffffffffu, nd);
             if (ndup) {
                 const u32 dist = J - ndup;       // |S| after this round
                 if (!TU && dist < k) return J + (k - dist);
                 // compact the distinct values through shared memory, then store
-                u32 keep = 0;
-#pragma unroll
-                for (int i = 0; i < E; ++i) {
-                    const u32 p = p0 + i;
-                    keep += p >= h && p < h + J && !(p > h && y[i] == (i ? y[i - 1] : prv));
-                }
+                // (this lane keeps its positions in [h, h + J) but its duplicates)
+                const u32 klo = max(p0, h), khi = min(p0 + (u32)E, h + J);
+                const u32 keep = (khi > klo ? khi - klo : 0u) - nd;
                 u32 o = h + warp_excl_scan(keep, lane);
                 __syncwarp();
 #pragma unroll
