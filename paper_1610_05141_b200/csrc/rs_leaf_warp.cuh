@@ -703,17 +703,14 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
             if (ndup) {
                 const u32 dist = J - ndup;       // |S| after this round
                 if (!TU && dist < k) return J + (k - dist);
-                // compact the distinct values through shared memory, then store
-                // (this lane keeps its positions in [h, h + J) but its duplicates)
-                const u32 klo = max(p0, h), khi = min(p0 + (u32)E, h + J);
-                const u32 keep = (khi > klo ? khi - klo : 0u) - nd;
-                u32 o = h + warp_excl_scan(keep, lane);
+                // compact the distinct values through shared memory, then store:
+                // every position but the duplicates -- the pads stay at [0, h), the
+                // distinct draws land at [h, h + |S|), the sentinels above (unread)
+                u32 o = warp_excl_scan((u32)E - nd, lane);
                 __syncwarp();
 #pragma unroll
-                for (int i = 0; i < E; ++i) {
-                    const u32 p = p0 + i;
-                    if (p >= h && p < h + J && !(p > h && y[i] == (i ? y[i - 1] : prv))) sh.keys[o++] = y[i];
-                }
+                for (int i = 0; i < E; ++i)
+                    if (!(p0 + i > h && y[i] == (i ? y[i - 1] : prv))) sh.keys[o++] = y[i];
                 __syncwarp();
                 if (dist < k) return WL_TOPUP | dist;      // the caller tops the set up (wl_topup)
                 if (GR) { wl_store_edges(sh, d0, h, k, base, gV, lane); return 0; }
