@@ -693,12 +693,16 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
         for (int i = 1; i < E; ++i) m4[i & 3] = min(m4[i & 3], y[i] - y[i - 1]);
         const u32 md = min(min(m4[0], m4[1]), min(m4[2], m4[3]));
         if (__any_sync(0xffffffffu, md == 0u)) {
-            u32 nd = 0;
+            // exact count: distinct neighbours as min(difference, 1) (sorted:
+            // differences >= 0), two per three-input add; the sentinels are
+            // distinct and above every key, the pads 0, 1, 2 distinct, so only
+            // lane 0's first draw equal to its last pad is not a duplicate
+            u32 n4[4] = {lane ? min(y[0] - prv, 1u) : 1u, 0u, 0u, 0u};
 #pragma unroll
-            for (int i = 0; i < E; ++i) {
-                const u32 p = p0 + i;
-                nd += p > h && y[i] == (i ? y[i - 1] : prv);   // (sentinels: distinct, above every key)
-            }
+            for (int i = 1; i < E; i += 2)
+                n4[(i >> 1) & 3] += min(y[i] - y[i - 1], 1u) + (i + 1 < E ? min(y[i + 1] - y[i], 1u) : 1u);
+            u32 nd = (u32)E + 1u - ((n4[0] + n4[1]) + (n4[2] + n4[3]));
+            if (lane == 0 && h) nd -= h == 1 ? y[1] == y[0] : h == 2 ? y[2] == y[1] : y[3] == y[2];
             const u32 ndup = __reduce_add_sync(0xffffffffu, nd);
             if (ndup) {
                 const u32 dist = J - ndup;       // |S| after this round
