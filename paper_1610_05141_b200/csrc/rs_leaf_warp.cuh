@@ -771,14 +771,16 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
     }
     const u32 tg = (end - 1) & ~3u;               // tail group start (if partial, and not the head)
     if ((end & 3u) && tg >= 4 && lane == tg / E) {
+        // the group's three values selected first (a select chain), then ONE
+        // store sequence: this rarely-run code stays small
         const u32 mt = tg - p0;
+        u32 v0 = y[0], v1 = y[1], v2 = y[2];
 #pragma unroll
-        for (int m = 0; m < E; m += 4)
-            if ((u32)m == mt) {
-#pragma unroll
-                for (int t = 0; t < 3; ++t)
-                    if (tg + t < end) d0[tg + t] = out_word_t<GR>(base + y[m + t], gV);
-            }
+        for (int m = 4; m < E; m += 4)
+            if ((u32)m == mt) { v0 = y[m]; v1 = y[m + 1]; v2 = y[m + 2]; }
+        d0[tg] = out_word_t<GR>(base + v0, gV);                   // (tg < end: the group is partial)
+        if (tg + 1 < end) d0[tg + 1] = out_word_t<GR>(base + v1, gV);
+        if (tg + 2 < end) d0[tg + 2] = out_word_t<GR>(base + v2, gV);
     }
     __syncwarp();
     return 0;
