@@ -545,6 +545,7 @@ __device__ __forceinline__ bool wl_topup(const WarpLeaf &sh, const RoundKeys &K,
         dr.block<P2>(K, (j0 + lane) >> 2, v);
         const u32 w = (j0 + lane) & 3u;
         const u32 xl = w == 0 ? v[0] : w == 1 ? v[1] : w == 2 ? v[2] : v[3];
+#pragma unroll 1
         for (u32 t = 0; t < 32 && nv < need; ++t) {
             const u32 x = __shfl_sync(0xffffffffu, xl, t);
             u32 lo = 0, hi = dist;                       // lower_bound(ks, x)
@@ -608,10 +609,12 @@ __device__ __forceinline__ bool wl_topup(const WarpLeaf &sh, const RoundKeys &K,
     for (u32 i0 = 0; i0 < dist; i0 += 32) {         // warp-uniform trip count (shuffles inside)
         const u32 i = i0 + lane;
         u32 sft = (r0 <= i) + (r1 <= i) + (r2 <= i) + (r3 <= i);
+#pragma unroll 1
         for (u32 t = 4; t < nv; ++t) sft += __shfl_sync(0xffffffffu, mr, t) <= i;
         if (i < dist) d0[h + i + sft] = out_word_t<GR>(base + ks[i], gV);
     }
     u32 sft = 0;
+#pragma unroll 1
     for (u32 t = 0; t < nv; ++t) sft += __shfl_sync(0xffffffffu, mv, t) < mv;
     if (lane < nv) d0[h + mr + sft] = out_word_t<GR>(base + mv, gV);
     __syncwarp();
@@ -631,6 +634,7 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
     {   // sentinels WL_SENT0 + p above the last draw: distinct, larger than any key
         const u32 s0 = h + J, s4 = (s0 + 3) & ~3u;
         if (lane < s4 - s0 && s0 + lane < 32u * E) sh.keys[s0 + lane] = WL_SENT0 + s0 + lane;
+#pragma unroll 1
         for (u32 p = s4 + 4 * lane; p < 32u * E; p += 128)
             *reinterpret_cast<uint4 *>(&sh.keys[p]) =
                 make_uint4(WL_SENT0 + p, WL_SENT0 + p + 1, WL_SENT0 + p + 2, WL_SENT0 + p + 3);
