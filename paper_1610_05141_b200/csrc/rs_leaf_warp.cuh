@@ -330,19 +330,32 @@ __device__ __forceinline__ u32 wl_count_reg(WarpLeaf &sh, const RoundKeys &K, co
                                             u32 lane, u32 (&x)[WL_E1])
 {
     constexpr int NB = WL_E1 / 4;
+    // group m = draws [128 m, 128 m + 128): full groups straight from the
+    // unrolled loop; the one partial group (J mod 128 != 0) after it, its
+    // draws selected out of x -- one copy of the per-draw tests (this kernel
+    // is instruction-fetch sensitive); groups beyond J are not generated
 #pragma unroll
     for (int m = 0; m < NB; ++m) {
-        const u32 q = lane + 32u * m;
-        if (POW2) dr.block_pow2(K, q, &x[4 * m]);
-        else dr.d.block(q, &x[4 * m]);
-        if (128u * m + 127u < J) {               // every lane's four draws count
+        if (128u * m < J) {
+            const u32 q = lane + 32u * m;
+            if (POW2) dr.block_pow2(K, q, &x[4 * m]);
+            else dr.d.block(q, &x[4 * m]);
+            if (128u * m + 127u < J) {
 #pragma unroll
-            for (int t = 0; t < 4; ++t) atomicAdd(&sh.cnt[wl_bkt(x[4 * m + t], M)], 1u);
-        } else {
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-                if (4 * q + t < J) atomicAdd(&sh.cnt[wl_bkt(x[4 * m + t], M)], 1u);
+                for (int t = 0; t < 4; ++t) atomicAdd(&sh.cnt[wl_bkt(x[4 * m + t], M)], 1u);
+            }
         }
+    }
+    const u32 mp = J >> 7;
+    if ((J & 127u) && mp < (u32)NB) {
+        u32 v[4] = {x[0], x[1], x[2], x[3]};
+#pragma unroll
+        for (int m = 1; m < NB; ++m)
+            if ((u32)m == mp) { v[0] = x[4 * m]; v[1] = x[4 * m + 1]; v[2] = x[4 * m + 2]; v[3] = x[4 * m + 3]; }
+        const u32 q = lane + 32u * mp;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (4 * q + t < J) atomicAdd(&sh.cnt[wl_bkt(v[t], M)], 1u);
     }
     __syncwarp();
     u32 *cl = sh.cnt + 33 * lane;
@@ -378,26 +391,36 @@ __device__ __forceinline__ void wl_scatter_reg(WarpLeaf &sh, u32 J, u32 h, u32 M
     constexpr int NB = WL_E1 / 4;
     constexpr int GB = RS_WL_GB;
     static_assert(NB % GB == 0, "group size");
+    // full GB-groups of groups from the unrolled loop; the rest (at most GB
+    // groups, the last one partial) one group at a time after it, each
+    // group's draws selected out of x: one copy of the per-draw tests
+    u32 mr0 = 0;                                 // first group not in a full GB-group
 #pragma unroll
     for (int m0 = 0; m0 < NB; m0 += GB) {
-        u32 pos[4 * GB];
-        if (128u * (m0 + GB - 1) + 127u < J) {   // the group's draws all exist for every lane
+        if (128u * (m0 + GB - 1) + 127u < J) {   // the GB-group's draws all exist for every lane
+            u32 pos[4 * GB];
 #pragma unroll
             for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) pos[e - 4 * m0] = atomicAdd(&sh.cnt[wl_bkt(x[e], M)], 1u);
             // atomics first, stores after (smem stores and atomics may alias as far
             // as the compiler knows: interleaving would serialise every round trip)
 #pragma unroll
             for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) { RS_CHK(h + pos[e - 4 * m0] < (u32)WL_CAP); kh[pos[e - 4 * m0]] = x[e]; }
-        } else if (128u * m0 < J) {
-#pragma unroll
-            for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) {
-                const u32 j = 4 * (lane + 32u * (e >> 2)) + (e & 3);
-                pos[e - 4 * m0] = j < J ? atomicAdd(&sh.cnt[wl_bkt(x[e], M)], 1u) : (u32)WL_CAP;
-            }
-#pragma unroll
-            for (int e = 4 * m0; e < 4 * (m0 + GB); ++e)
-                if (pos[e - 4 * m0] != (u32)WL_CAP) { RS_CHK(h + pos[e - 4 * m0] < (u32)WL_CAP); kh[pos[e - 4 * m0]] = x[e]; }
+            mr0 = m0 + GB;
         }
+    }
+#pragma unroll 1
+    for (u32 m = mr0; m < mr0 + GB && 128u * m < J; ++m) {
+        u32 v[4] = {x[0], x[1], x[2], x[3]};
+#pragma unroll
+        for (int mm = 1; mm < NB; ++mm)
+            if ((u32)mm == m) { v[0] = x[4 * mm]; v[1] = x[4 * mm + 1]; v[2] = x[4 * mm + 2]; v[3] = x[4 * mm + 3]; }
+        u32 pos[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            pos[t] = 4 * (lane + 32u * m) + t < J ? atomicAdd(&sh.cnt[wl_bkt(v[t], M)], 1u) : (u32)WL_CAP;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (pos[t] != (u32)WL_CAP) { RS_CHK(h + pos[t] < (u32)WL_CAP); kh[pos[t]] = v[t]; }
     }
     __syncwarp();
 }
