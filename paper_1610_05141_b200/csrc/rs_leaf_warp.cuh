@@ -451,6 +451,7 @@ __device__ __forceinline__ void st_v4_base_if(bool pred, u64 *p, u64 base, u32 a
 }
 
 // Step 3: every draw of the round to its bucket's next position (+ h).
+template <bool REM = true>   // REM: the partial groups in one after-loop copy (smaller code; WR measured slower)
 __device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const RoundKeys &K, const WDrawer &dr, u32 J, u32 h, int shb, u32 lane)
 {
     u32 *kh = sh.keys + h;
@@ -500,12 +501,13 @@ __device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const RoundKeys &K, con
     // would serialise every atomic's round trip.
     constexpr int GB = RS_WL_GB;
     static_assert(NB % GB == 0, "group size");
+    u32 mr0 = 0;                                 // first group not in a full GB-group
 #pragma unroll
     for (int m0 = 0; m0 < NB; m0 += GB) {
-        u32 pos[4 * GB];
-        // the group's draws all exist for every lane: no per-draw test
+        // the GB-group's draws all exist for every lane: no per-draw test
         const bool full = 4 * (31u + 32u * (m0 + GB - 1)) + 3 < J;
         if (full) {
+            u32 pos[4 * GB];
 #pragma unroll
             for (int e = 4 * m0; e < 4 * (m0 + GB); ++e)
 #ifdef RS_EXP_NOSCATTER
@@ -515,16 +517,40 @@ __device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const RoundKeys &K, con
 #endif
 #pragma unroll
             for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) { RS_CHK(h + pos[e - 4 * m0] < (u32)WL_CAP); kh[pos[e - 4 * m0]] = x[e]; }
-        } else if (4 * (lane + 32u * m0) < J) {
-#pragma unroll
-            for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) {
-                const u32 j = 4 * (lane + 32u * (e >> 2)) + (e & 3);
-                pos[e - 4 * m0] = j < J ? WL_POS(e) : (u32)WL_CAP;
-            }
-#pragma unroll
-            for (int e = 4 * m0; e < 4 * (m0 + GB); ++e)
-                if (pos[e - 4 * m0] != (u32)WL_CAP) { RS_CHK(h + pos[e - 4 * m0] < (u32)WL_CAP); kh[pos[e - 4 * m0]] = x[e]; }
+            mr0 = m0 + GB;
         }
+    }
+#if !RS_WL_RANK
+    // the rest (at most GB groups, the last partial) one group at a time, its
+    // draws selected out of x: one copy of the per-draw tests (code size)
+#pragma unroll 1
+    for (u32 m = mr0; REM && m < mr0 + GB && 128u * m < J; ++m) {
+        u32 v[4] = {x[0], x[1], x[2], x[3]};
+#pragma unroll
+        for (int mm = 1; mm < NB; ++mm)
+            if ((u32)mm == m) { v[0] = x[4 * mm]; v[1] = x[4 * mm + 1]; v[2] = x[4 * mm + 2]; v[3] = x[4 * mm + 3]; }
+        u32 pos[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            pos[t] = 4 * (lane + 32u * m) + t < J ? atomicAdd(&sh.cnt[wl_word(v[t] >> shb)], 1u) : (u32)WL_CAP;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (pos[t] != (u32)WL_CAP) { RS_CHK(h + pos[t] < (u32)WL_CAP); kh[pos[t]] = v[t]; }
+    }
+#endif
+#pragma unroll
+    for (int m0 = 0; m0 < NB; m0 += GB) {
+        if (REM && !RS_WL_RANK) break;          // (handled above)
+        if ((u32)m0 < mr0 || !(4 * (lane + 32u * m0) < J)) continue;
+        u32 pos[4 * GB];
+#pragma unroll
+        for (int e = 4 * m0; e < 4 * (m0 + GB); ++e) {
+            const u32 j = 4 * (lane + 32u * (e >> 2)) + (e & 3);
+            pos[e - 4 * m0] = j < J ? WL_POS(e) : (u32)WL_CAP;
+        }
+#pragma unroll
+        for (int e = 4 * m0; e < 4 * (m0 + GB); ++e)
+            if (pos[e - 4 * m0] != (u32)WL_CAP) kh[pos[e - 4 * m0]] = x[e];
     }
 #undef WL_POS
 #endif
@@ -891,7 +917,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)   // CS: CTA-span
                     __syncwarp();
                 } else if (J + h <= 32u * WL_E1) {
                     RS_TS(ts0);
-                    wl_scatter(sh, a.rk, dr, J, h, shb, lane);
+                    wl_scatter<!WR>(sh, a.rk, dr, J, h, shb, lane);
                     RS_TS(ts1);
                     RS_ACC(2, ts0, ts1);
                     res = wl_finish<WL_E1, WR, GR, TU>(sh, J, k, h, P, SMST ? 0 : base, SMST ? nullptr : dst, lane, a.gV);
@@ -902,7 +928,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)   // CS: CTA-span
                     wl_clear(sh, lane);         // larger leaves go to the CTA kernel (measured faster than a second, 44-position instantiation)
                     __syncwarp();
 #else
-                    wl_scatter(sh, a.rk, dr, J, h, shb, lane);
+                    wl_scatter<!WR>(sh, a.rk, dr, J, h, shb, lane);
                     res = wl_finish<WL_E2, WR, GR, TU>(sh, J, k, h, P, base, dst, lane, a.gV);
 #endif
                 }
