@@ -80,17 +80,37 @@ __device__ __forceinline__ void ww_scatter(WarpLeafW &sh, u32 J, u32 h, u32 lane
     }
     __syncwarp();
     u32 *kh = sh.w.keys + h, *lh = sh.lows + h;
+    // full groups (every lane's four draws exist) unrolled without per-draw
+    // tests; the one partial group after the loop, its draws selected out of
+    // x / l: one copy of the tests (the warp kernels are instruction-fetch
+    // sensitive)
 #pragma unroll
     for (int m = 0; m < NB; ++m) {
+        if (128u * m + 127u < J) {
+            u32 pos[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) pos[t] = atomicAdd(&sh.w.cnt[wl_word(x[4 * m + t] >> (WW_KEYBITS - WL_LOGB))], 1u);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) { RS_CHK(h + pos[t] < (u32)WL_CAP); kh[pos[t]] = x[4 * m + t]; lh[pos[t]] = l[4 * m + t]; }
+        }
+    }
+    const u32 mp = J >> 7;
+    if ((J & 127u) && mp < (u32)NB) {
+        u32 v[4] = {x[0], x[1], x[2], x[3]}, w[4] = {l[0], l[1], l[2], l[3]};
+#pragma unroll
+        for (int m = 1; m < NB; ++m)
+            if ((u32)m == mp) {
+                v[0] = x[4 * m]; v[1] = x[4 * m + 1]; v[2] = x[4 * m + 2]; v[3] = x[4 * m + 3];
+                w[0] = l[4 * m]; w[1] = l[4 * m + 1]; w[2] = l[4 * m + 2]; w[3] = l[4 * m + 3];
+            }
         u32 pos[4];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const u32 j = 4 * (lane + 32u * m) + t;
-            pos[t] = j < J ? atomicAdd(&sh.w.cnt[wl_word(x[4 * m + t] >> (WW_KEYBITS - WL_LOGB))], 1u) : (u32)WL_CAP;
-        }
+        for (int t = 0; t < 4; ++t)
+            pos[t] = 4 * (lane + 32u * mp) + t < J ? atomicAdd(&sh.w.cnt[wl_word(v[t] >> (WW_KEYBITS - WL_LOGB))], 1u)
+                                                   : (u32)WL_CAP;
 #pragma unroll
         for (int t = 0; t < 4; ++t)
-            if (pos[t] != (u32)WL_CAP) { RS_CHK(h + pos[t] < (u32)WL_CAP); kh[pos[t]] = x[4 * m + t]; lh[pos[t]] = l[4 * m + t]; }
+            if (pos[t] != (u32)WL_CAP) { RS_CHK(h + pos[t] < (u32)WL_CAP); kh[pos[t]] = v[t]; lh[pos[t]] = w[t]; }
     }
     __syncwarp();
 }
@@ -111,6 +131,7 @@ __device__ __forceinline__ bool ww_finish(WarpLeafW &sh, u32 J, u32 h, u32 P, u6
     if (lane < h) sh.w.keys[lane] = 0u;          // pads below the first draw (never above a key)
     {   // sentinels WL_SENT0 + p above the last draw: distinct, larger than any key
         const u32 s0 = h + J;
+#pragma unroll 1
         for (u32 p = s0 + lane; p < 32u * E; p += 32) sh.w.keys[p] = WL_SENT0 + p;
     }
     __syncwarp();
@@ -141,25 +162,40 @@ __device__ __forceinline__ bool ww_finish(WarpLeafW &sh, u32 J, u32 h, u32 P, u6
     const u32 p0 = E * lane;
     bool eq = false;
     const u32 prv = __shfl_up_sync(0xffffffffu, y[E - 1], 1);
-    eq |= lane > 0 && p0 > h && p0 < h + J && y[0] == prv;
+    eq |= lane > 0 && p0 > h && y[0] == prv;            // (sentinels: distinct, above every key)
 #pragma unroll
-    for (int i = 1; i < E; ++i) eq |= y[i] == y[i - 1] && p0 + i > h && p0 + i < h + J;
+    for (int i = 1; i < E; ++i) eq |= y[i] == y[i - 1] && p0 + i > h;
     if (__any_sync(0xffffffffu, eq)) return false;
     u64 *d0 = dst - h;                           // 32-byte aligned
     const u32 end = h + J;
+    // full 32-byte groups from registers; the partial head (positions 0..3,
+    // lane 0) and tail groups after, the tail's values selected first: one
+    // copy of the per-value stores
 #pragma unroll
     for (int m = 0; m < E; m += 4) {
         const u32 p = p0 + m;
-        u64 v[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) v[t] = base + (((u64)y[m + t] << shk) | pl[m + t]);
         if (p >= h && p + 4 <= end) {
-            st_v4(d0 + p, v[0], v[1], v[2], v[3]);
-        } else {
+            u64 v[4];
 #pragma unroll
-            for (int t = 0; t < 4; ++t)
-                if (p + t >= h && p + t < end) d0[p + t] = v[t];
+            for (int t = 0; t < 4; ++t) v[t] = base + (((u64)y[m + t] << shk) | pl[m + t]);
+            st_v4(d0 + p, v[0], v[1], v[2], v[3]);
         }
+    }
+    if (lane == 0 && (h || end < 4)) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if ((u32)t >= h && (u32)t < end) d0[t] = base + (((u64)y[t] << shk) | pl[t]);
+    }
+    const u32 tg = (end - 1) & ~3u;
+    if ((end & 3u) && tg >= 4 && lane == tg / E) {
+        const u32 mt = tg - p0;
+        u32 k0 = y[0], k1 = y[1], k2 = y[2], q0 = pl[0], q1 = pl[1], q2 = pl[2];
+#pragma unroll
+        for (int m = 4; m < E; m += 4)
+            if ((u32)m == mt) { k0 = y[m]; k1 = y[m + 1]; k2 = y[m + 2]; q0 = pl[m]; q1 = pl[m + 1]; q2 = pl[m + 2]; }
+        d0[tg] = base + (((u64)k0 << shk) | q0);
+        if (tg + 1 < end) d0[tg + 1] = base + (((u64)k1 << shk) | q1);
+        if (tg + 2 < end) d0[tg + 2] = base + (((u64)k2 << shk) | q2);
     }
     __syncwarp();
     return true;
