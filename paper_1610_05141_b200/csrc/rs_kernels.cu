@@ -278,8 +278,10 @@ namespace rs {
 // otherwise (about 1 draw in 2000 at rho = 0.01) G is evaluated exactly in
 // fp64 as CANON defines it (log_, IEEE division, floor).  Bit-exact either way.
 // ===========================================================================
+// (out of line: rare, and four inlined copies of log_ cost the Bernoulli
+// kernels instruction-cache space)
 template <typename T>
-__device__ __forceinline__ T skip_exact(double U, double lr, T r)
+__device__ __noinline__ T skip_exact(double U, double lr, T r)
 {
     const double G = floor_(log_(U) / lr);
     return G >= (double)r ? r + 1 : (T)G + 1;       // any G >= r ends the chain
