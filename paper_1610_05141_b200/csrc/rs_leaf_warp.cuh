@@ -408,12 +408,15 @@ __device__ __forceinline__ void wl_scatter_reg(WarpLeaf &sh, u32 J, u32 h, u32 M
             mr0 = m0 + GB;
         }
     }
-#pragma unroll 1
-    for (u32 m = mr0; m < mr0 + GB && 128u * m < J; ++m) {
-        u32 v[4] = {x[0], x[1], x[2], x[3]};
+    // (group mr0 + g: mr0 is a multiple of GB, so a (NB / GB)-way select)
 #pragma unroll
-        for (int mm = 1; mm < NB; ++mm)
-            if ((u32)mm == m) { v[0] = x[4 * mm]; v[1] = x[4 * mm + 1]; v[2] = x[4 * mm + 2]; v[3] = x[4 * mm + 3]; }
+    for (int g = 0; g < GB; ++g) {
+        const u32 m = mr0 + g;
+        if (128u * m >= J) break;
+        u32 v[4] = {x[4 * g], x[4 * g + 1], x[4 * g + 2], x[4 * g + 3]};
+#pragma unroll
+        for (int m0 = GB; m0 < NB; m0 += GB)
+            if ((u32)m0 == mr0) { v[0] = x[4 * (m0 + g)]; v[1] = x[4 * (m0 + g) + 1]; v[2] = x[4 * (m0 + g) + 2]; v[3] = x[4 * (m0 + g) + 3]; }
         u32 pos[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t)
