@@ -526,12 +526,14 @@ __device__ __forceinline__ void wl_scatter(WarpLeaf &sh, const RoundKeys &K, con
 #if !RS_WL_RANK
     // the rest (at most GB groups, the last partial) one group at a time, its
     // draws selected out of x: one copy of the per-draw tests (code size)
-#pragma unroll 1
-    for (u32 m = mr0; REM && m < mr0 + GB && 128u * m < J; ++m) {
-        u32 v[4] = {x[0], x[1], x[2], x[3]};
 #pragma unroll
-        for (int mm = 1; mm < NB; ++mm)
-            if ((u32)mm == m) { v[0] = x[4 * mm]; v[1] = x[4 * mm + 1]; v[2] = x[4 * mm + 2]; v[3] = x[4 * mm + 3]; }
+    for (int g = 0; g < GB; ++g) {
+        const u32 m = mr0 + g;
+        if (!REM || 128u * m >= J) break;
+        u32 v[4] = {x[4 * g], x[4 * g + 1], x[4 * g + 2], x[4 * g + 3]};
+#pragma unroll
+        for (int m0 = GB; m0 < NB; m0 += GB)
+            if ((u32)m0 == mr0) { v[0] = x[4 * (m0 + g)]; v[1] = x[4 * (m0 + g) + 1]; v[2] = x[4 * (m0 + g) + 2]; v[3] = x[4 * (m0 + g) + 3]; }
         u32 pos[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t)
@@ -920,7 +922,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)   // CS: CTA-span
                     __syncwarp();
                 } else if (J + h <= 32u * WL_E1) {
                     RS_TS(ts0);
-                    wl_scatter<!WR>(sh, a.rk, dr, J, h, shb, lane);
+                    wl_scatter<true>(sh, a.rk, dr, J, h, shb, lane);
                     RS_TS(ts1);
                     RS_ACC(2, ts0, ts1);
                     res = wl_finish<WL_E1, WR, GR, TU>(sh, J, k, h, P, SMST ? 0 : base, SMST ? nullptr : dst, lane, a.gV);
@@ -931,7 +933,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)   // CS: CTA-span
                     wl_clear(sh, lane);         // larger leaves go to the CTA kernel (measured faster than a second, 44-position instantiation)
                     __syncwarp();
 #else
-                    wl_scatter<!WR>(sh, a.rk, dr, J, h, shb, lane);
+                    wl_scatter<true>(sh, a.rk, dr, J, h, shb, lane);
                     res = wl_finish<WL_E2, WR, GR, TU>(sh, J, k, h, P, base, dst, lane, a.gV);
 #endif
                 }
