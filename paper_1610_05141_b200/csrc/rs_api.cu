@@ -26,6 +26,9 @@ int g_warp_cap = 0;                     // rs_set_option(RS_OPT_WARP_CAP): warp 
 #ifndef RS_WL_WOR_TU_ALL
 #define RS_WL_WOR_TU_ALL 1
 #endif
+#ifndef RS_WL_SD
+#define RS_WL_SD 1          // power-of-two WOR above the top-up cutoff: duplicate leaves to a second pass
+#endif
 #ifndef RS_WL_P2
 #define RS_WL_P2 1
 #endif
@@ -168,7 +171,7 @@ rs_status plan_node(int mode, u64 N, u64 n, u64 seed, int s, u64 idx, TreePlan &
     p.o_pong_off = o; o = align256(o + wmax * 8);
     p.o_leaf_cnt = o; o = align256(o + p.nleaves * 4);
     p.o_leaf_off = o; o = align256(o + p.nleaves * 8);
-    p.o_spill = o; o = align256(o + (p.nleaves + 4) * 4);   // status word, spill count, barrier, pad, spill list
+    p.o_spill = o; o = align256(o + (2 * p.nleaves + 8) * 4);   // header (8 words), spill list, duplicate list
     p.bytes = o;
     return RS_OK;
 }
@@ -241,7 +244,7 @@ bool run_fused(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t st)
     la.wcap = (u32)g_warp_cap;
     la.topup_max = (u32)g_topup_max;
     la.spill_n = status + 1;
-    la.spill = status + 4;
+    la.spill = status + 8;
     f.N = p.N; f.seed = p.seed; f.s = p.s; f.D = p.D;
     f.lb = depth < FUSED_LB ? depth : depth > FUSED_LB + RS_FUSED_CTA_LOG ? depth - RS_FUSED_CTA_LOG : FUSED_LB;
     la.span_log = (u32)f.lb;
@@ -263,7 +266,7 @@ bool run_fused(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t st)
     if (wide_sep) {                                             // the CTA kernel with u64 keys
         LeafArgs lb = la;
         lb.spill = nullptr; lb.spill_n = nullptr;
-        lb.list = status + 4; lb.list_n = status + 1;
+        lb.list = status + 8; lb.list_n = status + 1;
         void (*kern)(LeafArgs) = wr ? k_leaf_wr64 : k_leaf_wor64;
         const unsigned g2 = leaf_grid((const void *)kern, LEAF_NT, sizeof(SLeaf<u64>),
                                       p.nleaves < 2ull * 148 ? p.nleaves : 2ull * 148);
@@ -286,10 +289,10 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
                             (p.N >> p.D) >= (1ull << 11)) ||
                            (!p.comp && p.r_max > 0xfffff000ull && g_leaf_path != 1 && !p.gV);   // wide warp path
     (void)warp_path;
-    if (clear_status)      // status, spill count and the split's grid barrier in one memset
-        cudaMemsetAsync(status, 0, 16, st);
+    if (clear_status)      // the status header (status, spill / duplicate counts, barrier) in one memset
+        cudaMemsetAsync(status, 0, 32, st);
     else
-        cudaMemsetAsync(status + 1, 0, 12, st);
+        cudaMemsetAsync(status + 1, 0, 28, st);
     if (run_fused(p, out, ws, st)) return cuda_ok();
     u64 *ping_cnt = (u64 *)(ws + p.o_ping_cnt), *ping_off = (u64 *)(ws + p.o_ping_off);
     u64 *pong_cnt = (u64 *)(ws + p.o_pong_cnt), *pong_off = (u64 *)(ws + p.o_pong_off);
@@ -422,7 +425,7 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         // list that the CTA kernel completes right after (usually empty)
         u32 *spill_n = status + 1;        // zeroed above
         la.spill_n = spill_n;
-        la.spill = status + 4;
+        la.spill = status + 8;
         // leaves with many duplicates (r <= 2^21: >= 22 % of leaves) top the
         // distinct set up draw by draw instead of re-running a full round
         const bool tu = p.r_max <= WL_TU_RMAX;
@@ -454,16 +457,28 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
                                                ? (p2 ? (!tu && RS_WL_P2_PLAIN ? k_leaf_warp_wor_p2 : k_leaf_warp_wor_tu_p2)
                                                      : k_leaf_warp_wor_tu)
                                                : k_leaf_warp_wor);
+            // power-of-two WOR with duplicates rare (ranges above the top-up
+            // cutoff): the kernel without the duplicate path, then the top-up
+            // kernel over the leaves it listed (SD / LS, rs_leaf_warp.cuh)
+            const bool sd = !wr && p2 && !p.gV && !tu && RS_WL_SD && !(RS_WL_P2_PLAIN);
+            if (sd) wk = k_leaf_warp_wor_sd_p2;
+            la.dup = status + 8 + p.nleaves;
+            la.dup_n = status + 4;
             const int nw = (wr && p2) ? WR_WARPS : WL_WARPS;
             const size_t wsm = sizeof(WarpLeaf) * nw;
             const u64 wgrid = (p.nleaves + nw - 1) / nw;
             const unsigned g1 = leaf_grid((const void *)wk, 32 * nw, wsm, wgrid);
             wk<<<g1, 32 * nw, wsm, st>>>(la);
+            if (sd) {
+                ++t_launches;
+                const unsigned gl = leaf_grid((const void *)k_leaf_warp_wor_tu_p2_ls, 32 * WL_WARPS, wsm, wgrid);
+                k_leaf_warp_wor_tu_p2_ls<<<gl, 32 * WL_WARPS, wsm, st>>>(la);
+            }
         }
         ++t_launches;
         LeafArgs lb = la;
         lb.spill = nullptr; lb.spill_n = nullptr;
-        lb.list = status + 4; lb.list_n = spill_n;
+        lb.list = status + 8; lb.list_n = spill_n;
         kern = wr ? k_leaf_wr32 : k_leaf_wor32;
         sm = sizeof(SLeaf<u32>);
         const unsigned g2 = leaf_grid((const void *)kern, LEAF_NT, sm, 2ull * 148);
@@ -476,7 +491,7 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         // kernel with 64-bit keys completes the leaves it spills (ties)
         u32 *spill_n = status + 1;        // zeroed above
         la.spill_n = spill_n;
-        la.spill = status + 4;
+        la.spill = status + 8;
         void (*wk)(LeafArgs) = wr ? k_leaf_warp_wide_wr : k_leaf_warp_wide_wor;
         const size_t wsm = sizeof(WarpLeafW) * WW_WARPS;
         const unsigned g1 = leaf_grid((const void *)wk, 32 * WW_WARPS, wsm, (p.nleaves + WW_WARPS - 1) / WW_WARPS);
@@ -484,7 +499,7 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
         ++t_launches;
         LeafArgs lb = la;
         lb.spill = nullptr; lb.spill_n = nullptr;
-        lb.list = status + 4; lb.list_n = spill_n;
+        lb.list = status + 8; lb.list_n = spill_n;
         kern = wr ? k_leaf_wr64 : k_leaf_wor64;
         sm = sizeof(SLeaf<u64>);
         const unsigned g2 = leaf_grid((const void *)kern, LEAF_NT, sm, 2ull * 148);

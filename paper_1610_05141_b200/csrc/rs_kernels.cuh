@@ -191,6 +191,8 @@ struct LeafArgs {
     u32 lp_cr;             // LP kernels: ceil_log2 of the launch's largest leaf range (generation tag shift)
     u32 span_log;          // fused kernels: CTA c owns leaves [c << span_log, (c + 1) << span_log)
     u32 wcap;              // warp kernels: != 0 spills every leaf of more draws (RS_OPT_WARP_CAP, tests)
+    u32 *dup;              // SD warp kernels: leaves whose round drew a duplicate (appended) ...
+    u32 *dup_n;            //   ... and their count; the LS kernel then completes them
 };
 
 __global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_wor32(LeafArgs a);
@@ -223,6 +225,10 @@ __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu_
 constexpr int WR_WARPS = RS_WR_WARPS;   // warps per CTA of the power-of-two WR kernel
 __global__ void __launch_bounds__(32 * WR_WARPS, RS_WL_MINB) k_leaf_warp_wr_p2(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_p2(LeafArgs a);
+// power-of-two WOR for ranges where duplicates are rare: the main kernel without the duplicate
+// path (its leaves with a duplicate listed) + the top-up kernel over that list
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_sd_p2(LeafArgs a);
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu_p2_ls(LeafArgs a);
 // wide leaf ranges (> 2^32 - 4096): 31-bit keys + payload (rs_leaf_wide.cuh)
 #ifndef RS_WW_WARPS
 #define RS_WW_WARPS 12      // 167 registers (16 warps: 128 with 384 B spills; measured n = 2^28 leaf sweep 2.28 -> 1.90 ms)

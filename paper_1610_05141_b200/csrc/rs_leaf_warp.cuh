@@ -677,7 +677,9 @@ __device__ __forceinline__ bool wl_topup(const WarpLeaf &sh, const RoundKeys &K,
 
 constexpr u32 WL_TOPUP = 0x80000000u;      // wl_finish: "dist distinct values compacted, top up"
 
-template <int E, bool WR, bool GR, bool TU>
+constexpr u32 WL_DUPLIST = 0xfffffffeu;   // wl_finish (SD kernels): "duplicates: to the duplicate list"
+
+template <int E, bool WR, bool GR, bool TU, bool SD = false>
 __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 P_, u64 base,
                                          u64 *dst, u32 lane, u64 gV)   // (base, dst: unused if RS_WL_SMEMST)
 {
@@ -750,7 +752,8 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
 #pragma unroll
         for (int i = 1; i < E; ++i) m4[i & 3] = min(m4[i & 3], y[i] - y[i - 1]);
         const u32 md = min(min(m4[0], m4[1]), min(m4[2], m4[3]));
-        if (__any_sync(0xffffffffu, md == 0u)) {
+        if (SD && __any_sync(0xffffffffu, md == 0u)) return WL_DUPLIST;   // (or the first draw equal to the last pad)
+        if (!SD && __any_sync(0xffffffffu, md == 0u)) {
             // exact count: distinct neighbours as min(difference, 1) (sorted:
             // differences >= 0), two per three-input add; the sentinels are
             // distinct and above every key, the pads 0, 1, 2 distinct, so only
@@ -844,8 +847,13 @@ __device__ __forceinline__ u32 wl_finish(WarpLeaf &sh, u32 J, u32 k, u32 h, u32 
     return 0;
 }
 
-template <bool WR, bool GR, bool TU, bool P2 = false, bool CS = false, int NW = WL_WARPS>
-__device__ __forceinline__ void warp_leaves(const LeafArgs &a)   // CS: CTA-span leaf ranges (fused kernels)
+// CS: CTA-span leaf ranges (fused kernels).  SD: a leaf whose round has an
+// equal neighbour goes to the duplicate list (a.dup) instead of the duplicate
+// path, which is not compiled in (ranges where duplicates are rare: a smaller
+// kernel).  LS: the leaves of the duplicate list (the pass after an SD kernel).
+template <bool WR, bool GR, bool TU, bool P2 = false, bool CS = false, int NW = WL_WARPS, bool SD = false,
+          bool LS = false>
+__device__ __forceinline__ void warp_leaves(const LeafArgs &a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -853,25 +861,29 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)   // CS: CTA-span
     wl_clear(sh, lane);
     __syncwarp();
     const u64 stride = CS ? (u64)NW : (u64)gridDim.x * NW;
-    u64 L = CS ? ((u64)blockIdx.x << a.span_log) + wid : (u64)blockIdx.x * NW + wid;
-    const u64 Lend = CS ? min(a.nleaves, ((u64)blockIdx.x + 1) << a.span_log) : a.nleaves;
+    u64 I = CS ? ((u64)blockIdx.x << a.span_log) + wid : (u64)blockIdx.x * NW + wid;   // leaf (LS: list) index
+    const u64 Iend = LS ? (u64)*(volatile const u32 *)a.dup_n
+                        : CS ? min(a.nleaves, ((u64)blockIdx.x + 1) << a.span_log) : a.nleaves;
     // the next leaf's count / offset arrive by cp.async straight into shared
     // memory while this leaf is processed (no register stays live for them)
     const u32 s_k = (u32)__cvta_generic_to_shared(&sh.pf_k), s_off = (u32)__cvta_generic_to_shared(&sh.pf_off);
-    if (lane == 0 && L < Lend) {
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s_k), "l"(a.cnt + L) : "memory");
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s_off), "l"(a.off + L) : "memory");
+    if (lane == 0 && I < Iend) {
+        const u64 L0 = LS ? (u64)a.dup[I] : I;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s_k), "l"(a.cnt + L0) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s_off), "l"(a.off + L0) : "memory");
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    for (; L < Lend; L += stride) {
+    for (; I < Iend; I += stride) {
+        const u64 L = LS ? (u64)a.dup[I] : I;
         if (lane == 0) asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
         const u32 k = sh.pf_k;
         const u64 off = sh.pf_off;
         __syncwarp();
-        if (lane == 0 && L + stride < Lend) {   // prefetch the next leaf's count and offset
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s_k), "l"(a.cnt + L + stride) : "memory");
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s_off), "l"(a.off + L + stride) : "memory");
+        if (lane == 0 && I + stride < Iend) {   // prefetch the next leaf's count and offset
+            const u64 L1 = LS ? (u64)a.dup[I + stride] : I + stride;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s_k), "l"(a.cnt + L1) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s_off), "l"(a.off + L1) : "memory");
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
         if (k == 0) continue;
@@ -911,7 +923,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)   // CS: CTA-span
                     __syncwarp();
                 } else {
                     wl_scatter_reg(sh, J, h, M, lane, x);
-                    res = wl_finish<WL_E1, WR, GR, TU>(sh, J, k, h, P, SMST ? 0 : base, SMST ? nullptr : dst, lane, a.gV);
+                    res = wl_finish<WL_E1, WR, GR, TU, SD>(sh, J, k, h, P, SMST ? 0 : base, SMST ? nullptr : dst, lane, a.gV);
                 }
             }
             } else {
@@ -925,7 +937,7 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)   // CS: CTA-span
                     wl_scatter<true>(sh, a.rk, dr, J, h, shb, lane);
                     RS_TS(ts1);
                     RS_ACC(2, ts0, ts1);
-                    res = wl_finish<WL_E1, WR, GR, TU>(sh, J, k, h, P, SMST ? 0 : base, SMST ? nullptr : dst, lane, a.gV);
+                    res = wl_finish<WL_E1, WR, GR, TU, SD>(sh, J, k, h, P, SMST ? 0 : base, SMST ? nullptr : dst, lane, a.gV);
                     RS_TS(ts2);
                     RS_ACC(5, ts1, ts2);
                 } else {
@@ -940,6 +952,10 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)   // CS: CTA-span
             }
             }
             if (res == 0) break;
+            if (SD && res == WL_DUPLIST) {      // the list pass (a top-up kernel) completes this leaf
+                if (lane == 0) a.dup[atomicAdd(a.dup_n, 1u)] = (u32)L;
+                break;
+            }
             if (res == 0xffffffffu) {           // the CTA kernel completes this leaf
                 if (lane == 0) a.spill[atomicAdd(a.spill_n, 1u)] = (u32)L;
                 break;
@@ -963,6 +979,8 @@ __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm(Lea
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm_tu(LeafArgs a) { warp_leaves<false, true, true>(a); }
 // every leaf range a power of two (N = 2^a): no Lemire rejection code at all
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu_p2(LeafArgs a) { warp_leaves<false, false, true, true>(a); }
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_sd_p2(LeafArgs a) { warp_leaves<false, false, true, true, false, WL_WARPS, true>(a); }
+__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu_p2_ls(LeafArgs a) { warp_leaves<false, false, true, true, false, WL_WARPS, false, true>(a); }
 __global__ void __launch_bounds__(32 * WR_WARPS, RS_WL_MINB) k_leaf_warp_wr_p2(LeafArgs a) { warp_leaves<true, false, false, true, false, WR_WARPS>(a); }
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_p2(LeafArgs a) { warp_leaves<false, false, false, true>(a); }
 
