@@ -460,7 +460,10 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
             // power-of-two WOR with duplicates rare (ranges above the top-up
             // cutoff): the kernel without the duplicate path, then the top-up
             // kernel over the leaves it listed (SD / LS, rs_leaf_warp.cuh)
-            const bool sd = !wr && p2 && !p.gV && !tu && RS_WL_SD && !(RS_WL_P2_PLAIN);
+            // (from r = 2^24: P(duplicate) ~ k^2 / 2r <= 3 %, below the ~3 % the
+            // smaller kernel saves on every leaf)
+            const bool sd = !wr && p2 && !p.gV && !tu && RS_WL_SD && !(RS_WL_P2_PLAIN) &&
+                            (p.N >> p.D) >= (1ull << 24);
             if (sd) wk = k_leaf_warp_wor_sd_p2;
             la.dup = status + 8 + p.nleaves;
             la.dup_n = status + 4;
