@@ -153,6 +153,23 @@ def test_warp_spill_path(N, n):
     _no_device_errors()
 
 
+# power-of-two WOR, leaf ranges >= 2^24, shard depth > 14: the warp kernel
+# without the duplicate path lists its leaves with an equal neighbour and the
+# top-up kernel completes them from the list (rs_leaf_warp.cuh SD / LS)
+@pytest.mark.parametrize("N,n", [(2 ** 40, 2 ** 25), (2 ** 41, 2 ** 25 + 12345)])
+def test_duplicate_list_path(N, n):
+    got = _np(rs.sample_wor(N, n, 9))
+    assert np.array_equal(got, O.sample_wor(N, n, 9))
+    rs.set_option(rs.OPT_FUSED, 0)
+    try:
+        sh = _np(rs.sample_wor_shard(N, n, 9, 2, 1))
+    finally:
+        rs.set_option(rs.OPT_FUSED, 1)
+    c, off = rs.shard_info(N, n, 9, 2, 1)
+    assert np.array_equal(sh, got[off:off + c])
+    _no_device_errors()
+
+
 # ---- with replacement --------------------------------------------------------
 
 WR_CASES = [(1, 5), (4, 1000), (2, 3), (100, 100), (2 ** 24, 2 ** 20), (10 ** 9 + 7, 100003),
