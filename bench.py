@@ -409,6 +409,8 @@ def run_native(args):
                 kname += "_tu"
             if mode in ("wor", "wr") and (N & (N - 1)) == 0:     # power-of-two N: the _p2 kernels
                 kname += "_p2"
+                if mode == "wor" and (N >> D) >= 2 ** 24:          # the kernel without the duplicate
+                    kname = "k_leaf_warp_wor_sd_p2"                # path (+ its listed-leaf pass)
         # shard trees of depth <= 14 on the warp paths: split + leaves in one
         # launch (rs_fused.cuh); its time is the "leaf" class, split_ms ~ 0
         if mode in ("wor", "wr") and not comp and kname.startswith("k_leaf_warp_") and \

@@ -14,7 +14,7 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/r
 python bench.py --steps 2 --warmup 1 --launch-list --no-e2e --no-cpu > gpurun_out/r2_ll_plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r2_launches.csv \
       python bench.py --steps 2 --warmup 1 --launch-list --no-e2e --no-cpu > gpurun_out/r2_ll_ncu.log 2>&1
-for spec in headline:k_leaf_warp_wor_tu_p2 cfg1:k_leaf_warp_wor_tu_p2 wr:k_leaf_warp_wr_p2 complement:k_leaf_bitmap_comp bernoulli:k_bernoulli headline:k_split_deep3 cfg1:k_split_coop cfg0:k_fused_wor_tu_p2 gnm:k_leaf_warp_gnm algb:k_bernoulli64d; do
+for spec in headline:k_leaf_warp_wor_sd_p2 cfg1:k_leaf_warp_wor_tu_p2 wr:k_leaf_warp_wr_p2 complement:k_leaf_bitmap_comp bernoulli:k_bernoulli headline:k_split_deep3 cfg1:k_split_coop cfg0:k_fused_wor_tu_p2 gnm:k_leaf_warp_gnm algb:k_bernoulli64d; do
   W=${spec%%:*}; K=${spec#*:}
   timeout 300 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --workload $W > gpurun_out/r2_plain_$W.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$K" -s 1 -c 1 -o /tmp/r2_full_${W}_${K} -f \
@@ -26,7 +26,7 @@ for spec in headline:k_leaf_warp_wor_tu_p2 cfg1:k_leaf_warp_wor_tu_p2 wr:k_leaf_
   ncu -i $R --page raw --csv > gpurun_out/r2_full_${W}_${K}_raw.csv 2>/dev/null
   ncu -i $R --page source --csv --print-source cuda,sass > gpurun_out/r2_full_${W}_${K}_source.csv 2>/dev/null
   gzip -f gpurun_out/r2_full_${W}_${K}_source.csv
-  if [ "$W" = headline ] && [ "$K" = k_leaf_warp_wor_tu_p2 ]; then cp $R gpurun_out/; fi
+  if [ "$W" = headline ] && [ "$K" = k_leaf_warp_wor_sd_p2 ]; then cp $R gpurun_out/; fi
 done
 timeout 600 python tools/sweep.py > gpurun_out/r2_sweep.txt 2>&1
 # the wide (u64-range) warp leaf at the sweep's n = 2^28 (N = 2^50)
