@@ -212,7 +212,13 @@ __global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_comp64(LeafArgs 
 // warps (independent leaves) per CTA: measured best at 16 (one 16-warp CTA per
 // SM) for the counting-sort kernel and at 8 for the bitmap kernel
 constexpr int WL_WARPS = RS_WL_WARPS;
-constexpr int WB_WARPS = 8;
+#ifndef RS_WB_WARPS
+#define RS_WB_WARPS 8
+#endif
+#ifndef RS_WB_MINB
+#define RS_WB_MINB 4         // 64 registers (a few spills): 4 CTAs of 8 warps per SM; measured cfg3a leaf 6.89 -> 6.50 ms
+#endif
+constexpr int WB_WARPS = RS_WB_WARPS;
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm(LeafArgs a);
@@ -276,10 +282,10 @@ __global__ void __launch_bounds__(32 * LP_WARPS, 1) k_leaf_lp_wr(LeafArgs a);
 #endif
 constexpr u64 WL_TU_RMAX = 1ull << RS_WL_TU_LOG;   // leaf ranges up to this take the top-up kernels
 // Warp-per-leaf bitmap kernels for leaf ranges r <= 2^15 (rs_leaf_bitmap.cuh).
-__global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_wor(LeafArgs a);
-__global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_comp(LeafArgs a);
-__global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_wor_g(LeafArgs a);
-__global__ void __launch_bounds__(32 * WB_WARPS) k_leaf_bitmap_comp_g(LeafArgs a);
+__global__ void __launch_bounds__(32 * WB_WARPS, RS_WB_MINB) k_leaf_bitmap_wor(LeafArgs a);
+__global__ void __launch_bounds__(32 * WB_WARPS, RS_WB_MINB) k_leaf_bitmap_comp(LeafArgs a);
+__global__ void __launch_bounds__(32 * WB_WARPS, RS_WB_MINB) k_leaf_bitmap_wor_g(LeafArgs a);
+__global__ void __launch_bounds__(32 * WB_WARPS, RS_WB_MINB) k_leaf_bitmap_comp_g(LeafArgs a);
 
 // ---------------------------------------------------------------------------
 // Bernoulli (row a9): one chunk per CTA (dynamic ticket order), geometric
