@@ -467,15 +467,16 @@ rs_status run_tree(const TreePlan &p, u64 *out, unsigned char *ws, cudaStream_t 
             if (sd) wk = k_leaf_warp_wor_sd_p2;
             la.dup = status + 8 + p.nleaves;
             la.dup_n = status + 4;
-            const int nw = (wr && p2) ? WR_WARPS : WL_WARPS;
+            const int nw = (wr && p2) ? WR_WARPS : sd ? SD_WARPS : WL_WARPS;
             const size_t wsm = sizeof(WarpLeaf) * nw;
             const u64 wgrid = (p.nleaves + nw - 1) / nw;
             const unsigned g1 = leaf_grid((const void *)wk, 32 * nw, wsm, wgrid);
             wk<<<g1, 32 * nw, wsm, st>>>(la);
             if (sd) {
                 ++t_launches;
-                const unsigned gl = leaf_grid((const void *)k_leaf_warp_wor_tu_p2_ls, 32 * WL_WARPS, wsm, wgrid);
-                k_leaf_warp_wor_tu_p2_ls<<<gl, 32 * WL_WARPS, wsm, st>>>(la);
+                const size_t lsm = sizeof(WarpLeaf) * WL_WARPS;
+                const unsigned gl = leaf_grid((const void *)k_leaf_warp_wor_tu_p2_ls, 32 * WL_WARPS, lsm, wgrid);
+                k_leaf_warp_wor_tu_p2_ls<<<gl, 32 * WL_WARPS, lsm, st>>>(la);
             }
         }
         ++t_launches;

@@ -233,7 +233,11 @@ __global__ void __launch_bounds__(32 * WR_WARPS, RS_WL_MINB) k_leaf_warp_wr_p2(L
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_p2(LeafArgs a);
 // power-of-two WOR for ranges where duplicates are rare: the main kernel without the duplicate
 // path (its leaves with a duplicate listed) + the top-up kernel over that list
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_sd_p2(LeafArgs a);
+#ifndef RS_SD_WARPS
+#define RS_SD_WARPS 16
+#endif
+constexpr int SD_WARPS = RS_SD_WARPS;   // warps per CTA of the duplicate-free kernel
+__global__ void __launch_bounds__(32 * SD_WARPS, RS_WL_MINB) k_leaf_warp_wor_sd_p2(LeafArgs a);
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu_p2_ls(LeafArgs a);
 // wide leaf ranges (> 2^32 - 4096): 31-bit keys + payload (rs_leaf_wide.cuh)
 #ifndef RS_WW_WARPS

@@ -979,7 +979,7 @@ __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm(Lea
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm_tu(LeafArgs a) { warp_leaves<false, true, true>(a); }
 // every leaf range a power of two (N = 2^a): no Lemire rejection code at all
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu_p2(LeafArgs a) { warp_leaves<false, false, true, true>(a); }
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_sd_p2(LeafArgs a) { warp_leaves<false, false, true, true, false, WL_WARPS, true>(a); }
+__global__ void __launch_bounds__(32 * SD_WARPS, RS_WL_MINB) k_leaf_warp_wor_sd_p2(LeafArgs a) { warp_leaves<false, false, true, true, false, SD_WARPS, true>(a); }
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu_p2_ls(LeafArgs a) { warp_leaves<false, false, true, true, false, WL_WARPS, false, true>(a); }
 __global__ void __launch_bounds__(32 * WR_WARPS, RS_WL_MINB) k_leaf_warp_wr_p2(LeafArgs a) { warp_leaves<true, false, false, true, false, WR_WARPS>(a); }
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_p2(LeafArgs a) { warp_leaves<false, false, false, true>(a); }
