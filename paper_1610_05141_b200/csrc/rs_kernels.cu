@@ -631,10 +631,7 @@ __device__ __forceinline__ void bernoulli_chunks(const BernArgs &a)
 constexpr int BG16 = RS_BG;                                           // chunks per ticket (u16 path)
 constexpr u32 BCAP16 = ((BG16 * 1024 + 10 * 32 * (BG16 < 4 ? 2 : BG16 / 2) + 63) / 64) * 64;
 constexpr int BNW16 = (BCAP16 * 2 * 2 * 4 <= 48 * 1024) ? 4 : (BCAP16 * 2 * 2 * 2 <= 48 * 1024) ? 2 : 1;
-#ifndef RS_BMINB
-#define RS_BMINB 1
-#endif
-__global__ void __launch_bounds__(32 * BNW16, RS_BMINB) k_bernoulli(BernArgs a) { bernoulli_chunks<u32, uint16_t, BG16, BCAP16, BNW16, false, false>(a); }
+__global__ void __launch_bounds__(32 * BNW16) k_bernoulli(BernArgs a) { bernoulli_chunks<u32, uint16_t, BG16, BCAP16, BNW16, false, false>(a); }
 __global__ void __launch_bounds__(32 * BNW16) k_bernoulli_g(BernArgs a) { bernoulli_chunks<u32, uint16_t, BG16, BCAP16, BNW16, true, false>(a); }
 // r <= 2^24: u32 positions; 2^24 < r <= 2^32: u64 position arithmetic, u32
 // positions buffered; RS_B32G chunks per ticket.  These chunk ranges mean

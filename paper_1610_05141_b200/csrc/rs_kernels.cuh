@@ -216,7 +216,13 @@ constexpr int WL_WARPS = RS_WL_WARPS;
 #define RS_WB_WARPS 8
 #endif
 #ifndef RS_WB_MINB
-#define RS_WB_MINB 4         // 64 registers (a few spills): 4 CTAs of 8 warps per SM; measured cfg3a leaf 6.89 -> 6.50 ms
+#define RS_WB_MINB 0         // 0: no minimum-blocks bound (ptxas' own choice, 80 registers: measured fastest, cfg3a
+                             // leaf 6.11 ms; an explicit bound of 1 generated slower code, 6.89; 4: 64 registers, 6.50)
+#endif
+#if RS_WB_MINB
+#define RS_WB_LB __launch_bounds__(32 * WB_WARPS, RS_WB_MINB)
+#else
+#define RS_WB_LB __launch_bounds__(32 * WB_WARPS)
 #endif
 constexpr int WB_WARPS = RS_WB_WARPS;
 __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor(LeafArgs a);
@@ -286,10 +292,10 @@ __global__ void __launch_bounds__(32 * LP_WARPS, 1) k_leaf_lp_wr(LeafArgs a);
 #endif
 constexpr u64 WL_TU_RMAX = 1ull << RS_WL_TU_LOG;   // leaf ranges up to this take the top-up kernels
 // Warp-per-leaf bitmap kernels for leaf ranges r <= 2^15 (rs_leaf_bitmap.cuh).
-__global__ void __launch_bounds__(32 * WB_WARPS, RS_WB_MINB) k_leaf_bitmap_wor(LeafArgs a);
-__global__ void __launch_bounds__(32 * WB_WARPS, RS_WB_MINB) k_leaf_bitmap_comp(LeafArgs a);
-__global__ void __launch_bounds__(32 * WB_WARPS, RS_WB_MINB) k_leaf_bitmap_wor_g(LeafArgs a);
-__global__ void __launch_bounds__(32 * WB_WARPS, RS_WB_MINB) k_leaf_bitmap_comp_g(LeafArgs a);
+__global__ void RS_WB_LB k_leaf_bitmap_wor(LeafArgs a);
+__global__ void RS_WB_LB k_leaf_bitmap_comp(LeafArgs a);
+__global__ void RS_WB_LB k_leaf_bitmap_wor_g(LeafArgs a);
+__global__ void RS_WB_LB k_leaf_bitmap_comp_g(LeafArgs a);
 
 // ---------------------------------------------------------------------------
 // Bernoulli (row a9): one chunk per CTA (dynamic ticket order), geometric

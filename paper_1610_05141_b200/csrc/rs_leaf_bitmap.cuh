@@ -132,9 +132,9 @@ __device__ __forceinline__ void bitmap_leaves(const LeafArgs &a)
     }
 }
 
-__global__ void __launch_bounds__(32 * WB_WARPS, RS_WB_MINB) k_leaf_bitmap_wor(LeafArgs a) { bitmap_leaves<false, false>(a); }
-__global__ void __launch_bounds__(32 * WB_WARPS, RS_WB_MINB) k_leaf_bitmap_comp(LeafArgs a) { bitmap_leaves<true, false>(a); }
-__global__ void __launch_bounds__(32 * WB_WARPS, RS_WB_MINB) k_leaf_bitmap_wor_g(LeafArgs a) { bitmap_leaves<false, true>(a); }
-__global__ void __launch_bounds__(32 * WB_WARPS, RS_WB_MINB) k_leaf_bitmap_comp_g(LeafArgs a) { bitmap_leaves<true, true>(a); }
+__global__ void RS_WB_LB k_leaf_bitmap_wor(LeafArgs a) { bitmap_leaves<false, false>(a); }
+__global__ void RS_WB_LB k_leaf_bitmap_comp(LeafArgs a) { bitmap_leaves<true, false>(a); }
+__global__ void RS_WB_LB k_leaf_bitmap_wor_g(LeafArgs a) { bitmap_leaves<false, true>(a); }
+__global__ void RS_WB_LB k_leaf_bitmap_comp_g(LeafArgs a) { bitmap_leaves<true, true>(a); }
 
 }  // namespace rs
