@@ -119,25 +119,25 @@ __device__ __forceinline__ void fused_spills(const LeafArgs &a)
     if (last) sample_leaves<K, WR, true>(a);
 }
 
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wor_tu(FusedArgs f)
+__global__ void RS_WL_LB(WL_WARPS) k_fused_wor_tu(FusedArgs f)
 { fused_split<false>(f); warp_leaves<false, false, true, false, true>(f.la); fused_spills<u32, false>(f.la); }
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wor_tu_p2(FusedArgs f)
+__global__ void RS_WL_LB(WL_WARPS) k_fused_wor_tu_p2(FusedArgs f)
 { fused_split<false>(f); warp_leaves<false, false, true, true, true>(f.la); fused_spills<u32, false>(f.la); }
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wr(FusedArgs f)
+__global__ void RS_WL_LB(WL_WARPS) k_fused_wr(FusedArgs f)
 { fused_split<true>(f); warp_leaves<true, false, false, false, true>(f.la); fused_spills<u32, true>(f.la); }
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wr_p2(FusedArgs f)
+__global__ void RS_WL_LB(WL_WARPS) k_fused_wr_p2(FusedArgs f)
 { fused_split<true>(f); warp_leaves<true, false, false, true, true>(f.la); fused_spills<u32, true>(f.la); }
 // Wide leaves: with the spills in the kernel (one leaf per warp: the saved
 // launch matters) or left to a separate CTA launch (more leaves per warp: the
 // u64 spill routine inlined costs the leaf body registers, n = 2^24 229 ->
 // 245 us; the host picks)
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wor(FusedArgs f)
+__global__ void RS_WL_LB(WL_WARPS) k_fused_wide_wor(FusedArgs f)
 { fused_split<false>(f); warp_leaves_wide<false, true>(f.la); }
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wr(FusedArgs f)
+__global__ void RS_WL_LB(WL_WARPS) k_fused_wide_wr(FusedArgs f)
 { fused_split<true>(f); warp_leaves_wide<true, true>(f.la); }
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wor_s(FusedArgs f)
+__global__ void RS_WL_LB(WL_WARPS) k_fused_wide_wor_s(FusedArgs f)
 { fused_split<false>(f); warp_leaves_wide<false, true>(f.la); fused_spills<u64, false>(f.la); }
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wr_s(FusedArgs f)
+__global__ void RS_WL_LB(WL_WARPS) k_fused_wide_wr_s(FusedArgs f)
 { fused_split<true>(f); warp_leaves_wide<true, true>(f.la); fused_spills<u64, true>(f.la); }
 
 }  // namespace rs

@@ -206,6 +206,11 @@ __global__ void __launch_bounds__(LEAF_NT, RS_LEAF_MINB) k_leaf_comp64(LeafArgs 
 #ifndef RS_WL_MINB
 #define RS_WL_MINB 1
 #endif
+#if RS_WL_MINB
+#define RS_WL_LB(nw) __launch_bounds__(32 * (nw), RS_WL_MINB)
+#else
+#define RS_WL_LB(nw) __launch_bounds__(32 * (nw))
+#endif
 #ifndef RS_WL_WARPS
 #define RS_WL_WARPS 16
 #endif
@@ -225,26 +230,26 @@ constexpr int WL_WARPS = RS_WL_WARPS;
 #define RS_WB_LB __launch_bounds__(32 * WB_WARPS)
 #endif
 constexpr int WB_WARPS = RS_WB_WARPS;
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor(LeafArgs a);
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr(LeafArgs a);
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm(LeafArgs a);
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu(LeafArgs a);
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm_tu(LeafArgs a);
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu_p2(LeafArgs a);
+__global__ void RS_WL_LB(WL_WARPS) k_leaf_warp_wor(LeafArgs a);
+__global__ void RS_WL_LB(WL_WARPS) k_leaf_warp_wr(LeafArgs a);
+__global__ void RS_WL_LB(WL_WARPS) k_leaf_warp_gnm(LeafArgs a);
+__global__ void RS_WL_LB(WL_WARPS) k_leaf_warp_wor_tu(LeafArgs a);
+__global__ void RS_WL_LB(WL_WARPS) k_leaf_warp_gnm_tu(LeafArgs a);
+__global__ void RS_WL_LB(WL_WARPS) k_leaf_warp_wor_tu_p2(LeafArgs a);
 #ifndef RS_WR_WARPS
 #define RS_WR_WARPS 16
 #endif
 constexpr int WR_WARPS = RS_WR_WARPS;   // warps per CTA of the power-of-two WR kernel
-__global__ void __launch_bounds__(32 * WR_WARPS, RS_WL_MINB) k_leaf_warp_wr_p2(LeafArgs a);
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_p2(LeafArgs a);
+__global__ void RS_WL_LB(WR_WARPS) k_leaf_warp_wr_p2(LeafArgs a);
+__global__ void RS_WL_LB(WL_WARPS) k_leaf_warp_wor_p2(LeafArgs a);
 // power-of-two WOR for ranges where duplicates are rare: the main kernel without the duplicate
 // path (its leaves with a duplicate listed) + the top-up kernel over that list
 #ifndef RS_SD_WARPS
 #define RS_SD_WARPS 16
 #endif
 constexpr int SD_WARPS = RS_SD_WARPS;   // warps per CTA of the duplicate-free kernel
-__global__ void __launch_bounds__(32 * SD_WARPS, RS_WL_MINB) k_leaf_warp_wor_sd_p2(LeafArgs a);
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu_p2_ls(LeafArgs a);
+__global__ void RS_WL_LB(SD_WARPS) k_leaf_warp_wor_sd_p2(LeafArgs a);
+__global__ void RS_WL_LB(WL_WARPS) k_leaf_warp_wor_tu_p2_ls(LeafArgs a);
 // wide leaf ranges (> 2^32 - 4096): 31-bit keys + payload (rs_leaf_wide.cuh)
 #ifndef RS_WW_WARPS
 #define RS_WW_WARPS 12      // 167 registers (16 warps: 128 with 384 B spills; measured n = 2^28 leaf sweep 2.28 -> 1.90 ms)
@@ -252,9 +257,14 @@ __global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu_
 #ifndef RS_WW_MINB
 #define RS_WW_MINB 1
 #endif
+#if RS_WW_MINB
+#define RS_WW_LB __launch_bounds__(32 * WW_WARPS, RS_WW_MINB)
+#else
+#define RS_WW_LB __launch_bounds__(32 * WW_WARPS)
+#endif
 constexpr int WW_WARPS = RS_WW_WARPS;   // warps per CTA of the wide kernels
-__global__ void __launch_bounds__(32 * WW_WARPS, RS_WW_MINB) k_leaf_warp_wide_wor(LeafArgs a);
-__global__ void __launch_bounds__(32 * WW_WARPS, RS_WW_MINB) k_leaf_warp_wide_wr(LeafArgs a);
+__global__ void RS_WW_LB k_leaf_warp_wide_wor(LeafArgs a);
+__global__ void RS_WW_LB k_leaf_warp_wide_wr(LeafArgs a);
 // Small trees: split + leaves in one launch (rs_fused.cuh); CTA c owns the
 // WL_WARPS leaves under node c at depth D - lb of the shard rooted at (s, idx).
 struct FusedArgs {
@@ -272,14 +282,14 @@ struct FusedArgs {
 #ifndef RS_FUSED_CTA_LOG
 #define RS_FUSED_CTA_LOG 7 // at most 2^7 CTAs (one wave of one 16-warp CTA per SM): deeper trees give each CTA more levels
 #endif
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wor_tu(FusedArgs f);
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wor_tu_p2(FusedArgs f);
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wr(FusedArgs f);
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wr_p2(FusedArgs f);
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wor(FusedArgs f);
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wr(FusedArgs f);
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wor_s(FusedArgs f);
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_fused_wide_wr_s(FusedArgs f);
+__global__ void RS_WL_LB(WL_WARPS) k_fused_wor_tu(FusedArgs f);
+__global__ void RS_WL_LB(WL_WARPS) k_fused_wor_tu_p2(FusedArgs f);
+__global__ void RS_WL_LB(WL_WARPS) k_fused_wr(FusedArgs f);
+__global__ void RS_WL_LB(WL_WARPS) k_fused_wr_p2(FusedArgs f);
+__global__ void RS_WL_LB(WL_WARPS) k_fused_wide_wor(FusedArgs f);
+__global__ void RS_WL_LB(WL_WARPS) k_fused_wide_wr(FusedArgs f);
+__global__ void RS_WL_LB(WL_WARPS) k_fused_wide_wor_s(FusedArgs f);
+__global__ void RS_WL_LB(WL_WARPS) k_fused_wide_wr_s(FusedArgs f);
 // Ordered linear-probing leaf kernels (rs_leaf_lp.cuh): the default WOR / WR path.
 #ifndef RS_LP_WARPS
 #define RS_LP_WARPS 16

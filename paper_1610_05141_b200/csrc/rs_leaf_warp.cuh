@@ -970,18 +970,18 @@ __device__ __forceinline__ void warp_leaves(const LeafArgs &a)
     }
 }
 
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor(LeafArgs a) { warp_leaves<false, false, false>(a); }
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wr(LeafArgs a) { warp_leaves<true, false, false>(a); }
+__global__ void RS_WL_LB(WL_WARPS) k_leaf_warp_wor(LeafArgs a) { warp_leaves<false, false, false>(a); }
+__global__ void RS_WL_LB(WL_WARPS) k_leaf_warp_wr(LeafArgs a) { warp_leaves<true, false, false>(a); }
 // small leaf ranges (many duplicates): the top-up instead of full rounds
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu(LeafArgs a) { warp_leaves<false, false, true>(a); }
+__global__ void RS_WL_LB(WL_WARPS) k_leaf_warp_wor_tu(LeafArgs a) { warp_leaves<false, false, true>(a); }
 // G(n, m) (NEXT-3): the WOR kernel with the edge decode fused into its stores
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm(LeafArgs a) { warp_leaves<false, true, false>(a); }
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_gnm_tu(LeafArgs a) { warp_leaves<false, true, true>(a); }
+__global__ void RS_WL_LB(WL_WARPS) k_leaf_warp_gnm(LeafArgs a) { warp_leaves<false, true, false>(a); }
+__global__ void RS_WL_LB(WL_WARPS) k_leaf_warp_gnm_tu(LeafArgs a) { warp_leaves<false, true, true>(a); }
 // every leaf range a power of two (N = 2^a): no Lemire rejection code at all
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu_p2(LeafArgs a) { warp_leaves<false, false, true, true>(a); }
-__global__ void __launch_bounds__(32 * SD_WARPS, RS_WL_MINB) k_leaf_warp_wor_sd_p2(LeafArgs a) { warp_leaves<false, false, true, true, false, SD_WARPS, true>(a); }
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_tu_p2_ls(LeafArgs a) { warp_leaves<false, false, true, true, false, WL_WARPS, false, true>(a); }
-__global__ void __launch_bounds__(32 * WR_WARPS, RS_WL_MINB) k_leaf_warp_wr_p2(LeafArgs a) { warp_leaves<true, false, false, true, false, WR_WARPS>(a); }
-__global__ void __launch_bounds__(32 * WL_WARPS, RS_WL_MINB) k_leaf_warp_wor_p2(LeafArgs a) { warp_leaves<false, false, false, true>(a); }
+__global__ void RS_WL_LB(WL_WARPS) k_leaf_warp_wor_tu_p2(LeafArgs a) { warp_leaves<false, false, true, true>(a); }
+__global__ void RS_WL_LB(SD_WARPS) k_leaf_warp_wor_sd_p2(LeafArgs a) { warp_leaves<false, false, true, true, false, SD_WARPS, true>(a); }
+__global__ void RS_WL_LB(WL_WARPS) k_leaf_warp_wor_tu_p2_ls(LeafArgs a) { warp_leaves<false, false, true, true, false, WL_WARPS, false, true>(a); }
+__global__ void RS_WL_LB(WR_WARPS) k_leaf_warp_wr_p2(LeafArgs a) { warp_leaves<true, false, false, true, false, WR_WARPS>(a); }
+__global__ void RS_WL_LB(WL_WARPS) k_leaf_warp_wor_p2(LeafArgs a) { warp_leaves<false, false, false, true>(a); }
 
 }  // namespace rs

@@ -257,7 +257,7 @@ __device__ __forceinline__ void warp_leaves_wide(const LeafArgs &a)   // CS: CTA
     }
 }
 
-__global__ void __launch_bounds__(32 * WW_WARPS, RS_WW_MINB) k_leaf_warp_wide_wor(LeafArgs a) { warp_leaves_wide<false, false, WW_WARPS>(a); }
-__global__ void __launch_bounds__(32 * WW_WARPS, RS_WW_MINB) k_leaf_warp_wide_wr(LeafArgs a) { warp_leaves_wide<true, false, WW_WARPS>(a); }
+__global__ void RS_WW_LB k_leaf_warp_wide_wor(LeafArgs a) { warp_leaves_wide<false, false, WW_WARPS>(a); }
+__global__ void RS_WW_LB k_leaf_warp_wide_wr(LeafArgs a) { warp_leaves_wide<true, false, WW_WARPS>(a); }
 
 }  // namespace rs
