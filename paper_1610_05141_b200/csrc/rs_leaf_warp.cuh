@@ -300,6 +300,9 @@ __device__ __forceinline__ u32 wl_scan(WarpLeaf &sh, u32 lane)
 #ifndef RS_WL_REG
 #define RS_WL_REG 0         // 1: draws stay in registers from the count to the scatter (no staging round trip) in every kernel
 #endif
+#ifndef RS_WL_GBR
+#define RS_WL_GBR RS_WL_GB  // scatter group of the register-resident path (measured 1 / 3 / 9: equal / best / 6 % slower)
+#endif
 #ifndef RS_WL_REG_WR
 #define RS_WL_REG_WR 1      // register-resident count/scatter in the power-of-two WR kernel (measured: 10.91 -> 10.16 ms once the kernels were slimmed; slower before)
 #endif
@@ -389,7 +392,7 @@ __device__ __forceinline__ void wl_scatter_reg(WarpLeaf &sh, u32 J, u32 h, u32 M
 {
     u32 *kh = sh.keys + h;
     constexpr int NB = WL_E1 / 4;
-    constexpr int GB = RS_WL_GB;
+    constexpr int GB = RS_WL_GBR;
     static_assert(NB % GB == 0, "group size");
     // full GB-groups of groups from the unrolled loop; the rest (at most GB
     // groups, the last one partial) one group at a time after it, each
