@@ -663,12 +663,18 @@ __device__ __forceinline__ bool wl_topup(const WarpLeaf &sh, const RoundKeys &K,
     const u32 r1 = __shfl_sync(0xffffffffu, lane < nv ? mr : 0xffffffffu, 1);
     const u32 r2 = __shfl_sync(0xffffffffu, lane < nv ? mr : 0xffffffffu, 2);
     const u32 r3 = __shfl_sync(0xffffffffu, lane < nv ? mr : 0xffffffffu, 3);
-    for (u32 i0 = 0; i0 < dist; i0 += 32) {         // warp-uniform trip count (shuffles inside)
-        const u32 i = i0 + lane;
-        u32 sft = (r0 <= i) + (r1 <= i) + (r2 <= i) + (r3 <= i);
+    if (nv == 1) {                                  // (the common case: one compare per value)
 #pragma unroll 1
-        for (u32 t = 4; t < nv; ++t) sft += __shfl_sync(0xffffffffu, mr, t) <= i;
-        if (i < dist) d0[h + i + sft] = out_word_t<GR>(base + ks[i], gV);
+        for (u32 i = lane; i < dist; i += 32) d0[h + i + (r0 <= i)] = out_word_t<GR>(base + ks[i], gV);
+    } else {
+#pragma unroll 1
+        for (u32 i0 = 0; i0 < dist; i0 += 32) {     // warp-uniform trip count (shuffles inside)
+            const u32 i = i0 + lane;
+            u32 sft = (r0 <= i) + (r1 <= i) + (r2 <= i) + (r3 <= i);
+#pragma unroll 1
+            for (u32 t = 4; t < nv; ++t) sft += __shfl_sync(0xffffffffu, mr, t) <= i;
+            if (i < dist) d0[h + i + sft] = out_word_t<GR>(base + ks[i], gV);
+        }
     }
     u32 sft = 0;
 #pragma unroll 1
